@@ -1,0 +1,392 @@
+#!/usr/bin/env python
+"""CD-SGD step throughput (grad Gelem/s: quantize + exchange + update) on 1..8 B200.
+
+A "step" is one CD-SGD round of every rank on its own synthetic fp32 gradient:
+K1 key-segmented 2-bit quantize (fp64 residual) -> NCCL allgather of packed codes
+(or, every k-th round, ncclAllReduce of the fp32 gradient) -> fused K2/K3 apply
+with the local update (paper Eq. 10/11). Default workload: the north-star
+ResNet-50-sized gradient (161 keys, 25,557,032 elements per rank), k = 4.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...   (one rank per GPU)
+
+Prints ONE JSON line on rank 0. `value` = N * n * K / (max over ranks of the
+device-timed K steps); `e2e` = the same metric through the public API with the
+gradient copied from pinned host memory every step and the round's grad-norm
+read back. `--impl reference` times the CPU port of the reference algorithm
+(oracle/, test infrastructure) on the host cores instead.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+METRIC = "CD-SGD step throughput (grad Gelem/s, quantize+exchange+update)"
+UNIT = "Gelem/s"
+FALLBACK_HBM_GBS = 6650.0
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=40)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--workload", default="resnet50", help="resnet50 | resnet20 | vgg16 | single:<n> | keys:a,b,..")
+    ap.add_argument("--k", type=int, default=4)
+    ap.add_argument("--alpha", type=float, default=0.5)
+    ap.add_argument("--cpu-seconds", type=float, default=12.0, help="budget of the cpu_baseline sample")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def env_rank():
+    return (int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")),
+            int(os.environ.get("LOCAL_RANK", "0")))
+
+
+def workload_desc(layout, name):
+    return f"{name}-sized gradient: {len(layout)} keys, {layout.total:,} fp32 elements per rank"
+
+
+# ----------------------------------------------------------------------------- clocks
+
+
+class ClockSampler:
+    """nvidia-smi sampling DURING the timed region (B200_PROFILING.md clocks line)."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.path = tempfile.mktemp(prefix="clocks_", suffix=".csv")
+        self.proc = None
+        self.gpu = gpu_index
+
+    def start(self):
+        try:
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-lms", "100",
+                 "-i", str(self.gpu)], stdout=self.fh, stderr=subprocess.DEVNULL)
+        except (OSError, FileNotFoundError):
+            self.proc = None
+        time.sleep(0.25)
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        time.sleep(0.15)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.fh.close()
+        sm, smax, reasons = [], [], set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for line in open(self.path):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax.append(float(parts[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        os.unlink(self.path)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- peaks / traffic
+
+
+def hbm_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        v = float(json.load(open(p))["hbm_gbs"])
+        return v, "measured (MEASURED_PEAKS.json hbm_gbs, torch copy)"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic(workload: str, kernel: str):
+    """Per-launch DRAM bytes of `kernel` from the committed ncu --set full summary, else None."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        return json.load(open(p))[workload][kernel]["dram_bytes_per_launch"]
+    except Exception:
+        return None
+
+
+# ----------------------------------------------------------------------------- CPU legs
+
+
+def cpu_sample_layout(layout, budget_elems):
+    """First keys of the layout totalling ~budget_elems (a bounded sample of the workload)."""
+    from paper_2106_10796_b200.layout import Layout
+
+    spans, tot = [], 0
+    for s in layout.spans:
+        if tot >= budget_elems and spans:
+            break
+        spans.append((s.name, s.length))
+        tot += s.length
+    return Layout(spans)
+
+
+def cpu_port_rounds(sizes, n_workers, k, alpha, rounds, seed=0, threads=None):
+    """Time `rounds` lock-step CD-SGD rounds of the CPU port; returns (seconds, kind, cores, impl)."""
+    from oracle import cpu_port
+
+    return cpu_port.time_rounds(sizes, n_workers, k, alpha, rounds, seed=seed, threads=threads)
+
+
+def cpu_baseline(layout, args, n_workers):
+    from oracle import cpu_port
+
+    sample = cpu_sample_layout(layout, 4_000_000)
+    # calibrate one round, then size the round count to the budget (whole k-periods)
+    t1, kind, cores, impl = cpu_port.time_rounds(sample.lengths, n_workers, args.k, args.alpha, 1)
+    rounds = max(args.k, int(args.cpu_seconds / max(t1, 1e-6)) // args.k * args.k)
+    secs, kind, cores, impl = cpu_port.time_rounds(sample.lengths, n_workers, args.k, args.alpha, rounds)
+    value = n_workers * sample.total * rounds / secs / 1e9
+    return {"value": value, "unit": UNIT, "cores": cores, "kind": kind,
+            "sample": f"{rounds} lock-step rounds x {n_workers} worker(s) on the first {len(sample)} keys "
+                      f"({sample.total:,} elements) of the {args.workload} layout, k={args.k}; {impl}; "
+                      f"{secs:.1f} s"}
+
+
+def run_reference(args):
+    """--impl reference: the reference algorithm's CPU port on the host cores, rank 0 only."""
+    rank, world, _ = env_rank()
+    if rank != 0:
+        return 0
+    from oracle import cpu_port
+    from paper_2106_10796_b200.layout import by_name
+
+    layout = by_name(args.workload)
+    n_workers = max(args.gpus, world)
+    sample = cpu_sample_layout(layout, 2_000_000)
+    t1, kind, cores, impl = cpu_port.time_rounds(sample.lengths, n_workers, args.k, args.alpha, 1)
+    # each step is a bounded sample sized so warmup+steps finish in ~2-3 minutes
+    per_step_budget = 150.0 / max(1, args.steps + args.warmup)
+    scale = max(0.05, min(1.0, per_step_budget / max(t1, 1e-6)))
+    sample = cpu_sample_layout(layout, int(sample.total * scale))
+    cpu_port.time_rounds(sample.lengths, n_workers, args.k, args.alpha, args.warmup)
+    secs, kind, cores, impl = cpu_port.time_rounds(sample.lengths, n_workers, args.k, args.alpha, args.steps)
+    value = n_workers * sample.total * args.steps / secs / 1e9
+    desc = (f"{args.steps} lock-step rounds x {n_workers} simulated workers on the first {len(sample)} keys "
+            f"({sample.total:,} elements) of the {args.workload} layout; {impl}")
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * secs / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+        "config": {"workload": workload_desc(layout, args.workload), "k": args.k, "alpha": args.alpha,
+                   "algo": "cdsgd", "parallelism": f"dp{n_workers} (simulated, host)"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind, "sample": desc},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ----------------------------------------------------------------------------- our arm
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2106_10796_b200 import _lib
+    from paper_2106_10796_b200.comm import Comm, share_unique_id
+    from paper_2106_10796_b200.engine import HyperParams
+    from paper_2106_10796_b200.layout import by_name
+    from paper_2106_10796_b200.worker import CDSGDWorker
+
+    rank, world, local = env_rank()
+    if world != args.gpus and world > 1:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    _lib.load()
+    layout = by_name(args.workload)
+    n, nw = layout.total, layout.n_words
+    hp = HyperParams(algo="cdsgd", workers=world, eta_global=0.1, eta_local=0.4, k=args.k, alpha=args.alpha,
+                     warmup_n=0)
+    comm = Comm(share_unique_id(rank), world, rank) if world > 1 else None
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(1000 + rank)
+    w0 = torch.randn(n, device=dev, generator=torch.Generator(device=dev).manual_seed(999))
+    pool = [0.3 * torch.randn(n, device=dev, generator=gen) for _ in range(2)]
+    wk = CDSGDWorker(layout, hp, w0, rank=rank, comm=comm, gnorm_ring=64)
+    stream = torch.cuda.current_stream(dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local])
+        torch.cuda.synchronize(dev)
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---------------- device-resident timed region
+    W, K = max(args.warmup, 3), args.steps
+    for i in range(W):
+        wk.step(pool[i % 2])
+    wk.join()
+    wk.check()
+    barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    l0 = _lib.launch_count()
+    wk.profile_begin()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for i in range(K):
+        wk.step(pool[(W + i) % 2])
+    wk.join()
+    ev1.record(stream)
+    ev1.synchronize()
+    launches = _lib.launch_count() - l0
+    prof = wk.profile_end()
+    clk = clocks.stop()
+    ms = max_over_ranks(ev0.elapsed_time(ev1))
+    wk.check()
+    value = world * n * K / (ms / 1e3) / 1e9
+
+    # ---------------- per-kernel roofline (algorithmic bytes / avg CUDA-event duration)
+    peak, peak_src = hbm_peak()
+    alg = {
+        "quantize": 4 * n + 8 * n + 8 * n + 4 * nw,
+        "apply_quant": 4 * n + 4 * n + 4 * n + 4 * n + world * 4 * nw,
+        "apply_full": 5 * 4 * n,
+        "local_update": 3 * 4 * n,
+    }
+    kernels = {}
+    for kname, nbytes in alg.items():
+        st = prof[kname]
+        if st["n"]:
+            avg_ms = st["ms"] / st["n"]
+            gbs = nbytes / (avg_ms / 1e3) / 1e9
+            kernels[kname] = {"launches": st["n"], "avg_us": 1e3 * avg_ms, "bytes_per_launch": nbytes,
+                              "bytes_per_elem": round(nbytes / n, 4), "achieved_gbs": gbs, "frac": gbs / peak,
+                              "share_of_step": st["ms"] / (ms if world == 1 else ev0.elapsed_time(ev1))}
+    dom = max(kernels, key=lambda k: prof[k]["ms"])
+    roof = {"bound": "hbm", "kernel": dom, "achieved": kernels[dom]["achieved_gbs"], "peak": peak, "unit": "GB/s",
+            "frac": kernels[dom]["achieved_gbs"] / peak, "traffic": ncu_traffic(args.workload, dom),
+            "algorithmic_bytes_per_launch": alg[dom], "peak_source": peak_src}
+    exch = None
+    if world > 1 and prof["exchange"]["n"]:
+        P = 4 * nw
+        n_comp = sum(1 for i in range(K) if wk.round_compressed(W + i))
+        n_full = K - n_comp
+        bus_bytes = n_comp * (world - 1) * P + n_full * 2 * (world - 1) / world * 4 * n
+        exch = {"calls": prof["exchange"]["n"], "total_ms": prof["exchange"]["ms"],
+                "bus_gbs": bus_bytes / (prof["exchange"]["ms"] / 1e3) / 1e9, "nvlink_peak_gbs": 900.0,
+                "allgather_bytes_per_rank": P, "allreduce_bytes": 4 * n}
+        exch["bus_frac"] = exch["bus_gbs"] / 900.0
+
+    # ---------------- end-to-end through the public API with host buffers
+    e2e = None
+    if not args.no_e2e:
+        host = [torch.empty(n, dtype=torch.float32, pin_memory=True) for _ in range(3)]
+        for i, h in enumerate(host):
+            h.copy_(pool[i % 2].cpu())
+        dbuf = [torch.empty(n, dtype=torch.float32, device=dev) for _ in range(3)]
+        norms = torch.zeros(K + 1, dtype=torch.float64, pin_memory=True)
+        cs = torch.cuda.Stream(dev)
+        copied = [torch.cuda.Event() for _ in range(3)]
+        done = [torch.cuda.Event() for _ in range(K)]
+
+        def prefetch(i):
+            s = i % 3
+            with torch.cuda.stream(cs):
+                if i >= 2:
+                    cs.wait_event(done[i - 2])  # slot last used by round i-3: free once round i-2 applied it
+                dbuf[s].copy_(host[s], non_blocking=True)
+                copied[s].record(cs)
+
+        wk.flush()
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t_start = wk.t
+        e0.record(stream)
+        prefetch(0)
+        for i in range(K):
+            if i + 1 < K:
+                prefetch(i + 1)
+            stream.wait_event(copied[i % 3])
+            wk.step(dbuf[i % 3])
+            if i > 0:  # round t-1 was applied inside this step: read its grad norm back
+                norms[i - 1].copy_(wk.gnorm[(t_start + i - 1) % wk.gnorm_ring], non_blocking=True)
+            done[i].record(stream)
+        wk.join()
+        e1.record(stream)
+        e1.synchronize()
+        ems = max_over_ranks(e0.elapsed_time(e1))
+        wk.check()
+        e2e = {"value": world * n * K / (ems / 1e3) / 1e9, "unit": UNIT, "h2d_bytes_per_step": 4 * n,
+               "d2h_bytes_per_step": 8, "ms_per_step": ems / K,
+               "path": "CDSGDWorker.step (public API -> C ABI) with the gradient copied from pinned host memory "
+                       "on a copy stream each step and the round's grad-norm read back to pinned host"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(layout, args, 1)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
+            "ms_per_step": ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic",
+            "config": {"workload": workload_desc(layout, args.workload), "layout": args.workload,
+                       "n_per_rank": n, "keys": len(layout), "k": args.k, "alpha": args.alpha, "algo": "cdsgd",
+                       "warmup_n": 0, "residual": "fp64 (bit-exact)", "weights": "fp32",
+                       "exchange": "ncclAllGather(packed codes); ncclAllReduce(fp32) every k-th round",
+                       "l2": f"inputs larger than L2: {(20 * n) / 2**20:.0f} MiB touched per step per rank",
+                       "parallelism": f"dp{world}"},
+            "roofline": roof, "kernels": kernels, "exchange": exch, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": launches, "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    wk.close()
+    if comm is not None:
+        comm.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,749 @@
+// cdsgd_b200.cu — C ABI, launch logic, NCCL exchange and the per-rank step
+// engine of the B200-native CD-SGD hot path. Declarations and the reference
+// interface each entry point replaces: include/cdsgd_b200.h.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <atomic>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
+#include "cdsgd_b200.h"
+#include "kernels.cuh"
+
+using namespace cdsgd;
+
+// ------------------------------------------------------------------ errors
+namespace {
+thread_local char g_err[1024] = "";
+std::atomic<uint64_t> g_launches{0};
+
+int fail(int code, const char* fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+    return code;
+}
+}  // namespace
+
+#define CUDA_TRY(expr)                                                                   \
+    do {                                                                                 \
+        cudaError_t e_ = (expr);                                                         \
+        if (e_ != cudaSuccess) return fail(CDSGD_ERR_CUDA, "%s: %s", #expr, cudaGetErrorString(e_)); \
+    } while (0)
+#define NCCL_TRY(expr)                                                                   \
+    do {                                                                                 \
+        ncclResult_t r_ = (expr);                                                        \
+        if (r_ != ncclSuccess) return fail(CDSGD_ERR_NCCL, "%s: %s", #expr, ncclGetErrorString(r_)); \
+    } while (0)
+#define LAUNCH_CHECK()                                                                   \
+    do {                                                                                 \
+        g_launches.fetch_add(1, std::memory_order_relaxed);                              \
+        cudaError_t e_ = cudaGetLastError();                                             \
+        if (e_ != cudaSuccess) return fail(CDSGD_ERR_CUDA, "kernel launch: %s", cudaGetErrorString(e_)); \
+    } while (0)
+
+// ------------------------------------------------------------------ device facts
+namespace {
+struct DeviceInfo {
+    int sms = 0;
+};
+DeviceInfo& dev_info() {
+    static thread_local DeviceInfo cache[16];
+    int d = 0;
+    cudaGetDevice(&d);
+    DeviceInfo& di = cache[d & 15];
+    if (di.sms == 0) {
+        cudaDeviceGetAttribute(&di.sms, cudaDevAttrMultiProcessorCount, d);
+        if (di.sms <= 0) di.sms = 148;
+    }
+    return di;
+}
+template <typename K>
+int resident_blocks(K kernel, int threads) {
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, 0) != cudaSuccess || per_sm < 1)
+        per_sm = 1;
+    return per_sm * dev_info().sms;
+}
+constexpr int THREADS = 256;
+constexpr int WARPS_PER_BLOCK = THREADS / 32;
+
+template <typename K>
+int tile_grid(K kernel, int64_t ntiles) {
+    const int64_t want = (ntiles + WARPS_PER_BLOCK - 1) / WARPS_PER_BLOCK;
+    const int64_t cap = resident_blocks(kernel, THREADS);
+    return static_cast<int>(want < cap ? (want > 0 ? want : 1) : cap);
+}
+template <typename K>
+int flat_grid(K kernel, int64_t work) {
+    const int64_t want = (work + THREADS - 1) / THREADS;
+    const int64_t cap = resident_blocks(kernel, THREADS);
+    return static_cast<int>(want < cap ? (want > 0 ? want : 1) : cap);
+}
+inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+}  // namespace
+
+// ------------------------------------------------------------------ layout
+struct cdsgd_layout {
+    int32_t nkeys = 0;
+    int64_t n = 0, nwords = 0, ntiles = 0;
+    std::vector<int64_t> eoff, woff, toff;
+    int64_t* dev = nullptr;  // [3 * (nkeys+1)]: eoff | woff | toff
+    int device = 0;
+    KeyTab tab() const {
+        KeyTab k;
+        k.eoff = dev;
+        k.woff = dev + (nkeys + 1);
+        k.toff = dev + 2 * (nkeys + 1);
+        k.nkeys = nkeys;
+        k.ntiles = ntiles;
+        return k;
+    }
+};
+
+extern "C" int cdsgd_abi_version(void) { return CDSGD_ABI_VERSION; }
+extern "C" const char* cdsgd_last_error(void) { return g_err; }
+extern "C" uint64_t cdsgd_launch_count(void) { return g_launches.load(); }
+
+extern "C" int cdsgd_layout_create(const int64_t* lengths, int32_t n_keys, cdsgd_layout** out) {
+    if (out == nullptr) return fail(CDSGD_ERR_ARG, "out is NULL");
+    *out = nullptr;
+    if (n_keys < 1 || lengths == nullptr) return fail(CDSGD_ERR_ARG, "layout needs at least one key");
+    cdsgd_layout* L = new cdsgd_layout();
+    L->nkeys = n_keys;
+    L->eoff.assign(n_keys + 1, 0);
+    L->woff.assign(n_keys + 1, 0);
+    L->toff.assign(n_keys + 1, 0);
+    for (int32_t k = 0; k < n_keys; ++k) {
+        if (lengths[k] < 1) {
+            delete L;
+            return fail(CDSGD_ERR_ARG, "key %d has non-positive length %lld", k, (long long)lengths[k]);
+        }
+        const int64_t w = (lengths[k] + 15) / 16;
+        L->eoff[k + 1] = L->eoff[k] + lengths[k];
+        L->woff[k + 1] = L->woff[k] + w;
+        L->toff[k + 1] = L->toff[k] + (w + TILE_WORDS - 1) / TILE_WORDS;
+    }
+    L->n = L->eoff[n_keys];
+    L->nwords = L->woff[n_keys];
+    L->ntiles = L->toff[n_keys];
+    cudaGetDevice(&L->device);
+    std::vector<int64_t> h;
+    h.insert(h.end(), L->eoff.begin(), L->eoff.end());
+    h.insert(h.end(), L->woff.begin(), L->woff.end());
+    h.insert(h.end(), L->toff.begin(), L->toff.end());
+    cudaError_t e = cudaMalloc(&L->dev, h.size() * sizeof(int64_t));
+    if (e == cudaSuccess) e = cudaMemcpy(L->dev, h.data(), h.size() * sizeof(int64_t), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+        if (L->dev) cudaFree(L->dev);
+        delete L;
+        return fail(CDSGD_ERR_CUDA, "layout upload: %s", cudaGetErrorString(e));
+    }
+    *out = L;
+    return CDSGD_OK;
+}
+
+extern "C" int cdsgd_layout_destroy(cdsgd_layout* L) {
+    if (L == nullptr) return CDSGD_OK;
+    if (L->dev) cudaFree(L->dev);
+    delete L;
+    return CDSGD_OK;
+}
+extern "C" int64_t cdsgd_layout_elems(const cdsgd_layout* L) { return L ? L->n : -1; }
+extern "C" int64_t cdsgd_layout_words(const cdsgd_layout* L) { return L ? L->nwords : -1; }
+extern "C" int32_t cdsgd_layout_keys(const cdsgd_layout* L) { return L ? L->nkeys : -1; }
+extern "C" int cdsgd_layout_offsets(const cdsgd_layout* L, int64_t* eoff, int64_t* woff) {
+    if (L == nullptr) return fail(CDSGD_ERR_ARG, "layout is NULL");
+    if (eoff) memcpy(eoff, L->eoff.data(), L->eoff.size() * sizeof(int64_t));
+    if (woff) memcpy(woff, L->woff.data(), L->woff.size() * sizeof(int64_t));
+    return CDSGD_OK;
+}
+
+// ------------------------------------------------------------------ codec entry points
+extern "C" int cdsgd_quantize(const cdsgd_layout* L, const void* grad, int32_t gdt, const double* r_in,
+                              double* r_out, uint32_t* words, double alpha, uint64_t* err, uint64_t tag,
+                              void* stream) {
+    if (L == nullptr) return fail(CDSGD_ERR_ARG, "layout is NULL");
+    if (!(alpha > 0.0)) return fail(CDSGD_ERR_ARG, "threshold alpha must be > 0");
+    if (L->n == 0) return CDSGD_OK;
+    if (!grad || !r_in || !r_out || !words) return fail(CDSGD_ERR_ARG, "NULL buffer");
+    const KeyTab kt = L->tab();
+    if (gdt == CDSGD_F32) {
+        const int grid = tile_grid(k_quantize<float>, kt.ntiles);
+        k_quantize<float><<<grid, THREADS, 0, S(stream)>>>(static_cast<const float*>(grad), r_in, r_out, words,
+                                                            kt, alpha, err, tag);
+    } else if (gdt == CDSGD_F64) {
+        const int grid = tile_grid(k_quantize<double>, kt.ntiles);
+        k_quantize<double><<<grid, THREADS, 0, S(stream)>>>(static_cast<const double*>(grad), r_in, r_out,
+                                                             words, kt, alpha, err, tag);
+    } else {
+        return fail(CDSGD_ERR_ARG, "grad dtype must be CDSGD_F32 or CDSGD_F64");
+    }
+    LAUNCH_CHECK();
+    return CDSGD_OK;
+}
+
+extern "C" int cdsgd_dequantize_sum(const cdsgd_layout* L, const uint32_t* words, int32_t np, int64_t stride,
+                                    double alpha, double* out, uint64_t* err, void* stream) {
+    if (L == nullptr) return fail(CDSGD_ERR_ARG, "layout is NULL");
+    if (np < 1) return fail(CDSGD_ERR_ARG, "need at least one payload");
+    if (!(alpha > 0.0)) return fail(CDSGD_ERR_ARG, "threshold must be > 0");
+    if (L->n == 0) return CDSGD_OK;
+    const KeyTab kt = L->tab();
+    const int grid = tile_grid(k_dequant_sum, kt.ntiles);
+    k_dequant_sum<<<grid, THREADS, 0, S(stream)>>>(words, np, stride, kt, alpha, out, err);
+    LAUNCH_CHECK();
+    return CDSGD_OK;
+}
+
+extern "C" int cdsgd_aggregate_full(const void* grads, int32_t dt, int32_t nc, int64_t stride, int64_t n,
+                                    double* out, void* stream) {
+    if (nc < 1) return fail(CDSGD_ERR_ARG, "need at least one contribution");
+    if (n == 0) return CDSGD_OK;
+    if (dt == CDSGD_F32) {
+        k_aggregate_full<float><<<flat_grid(k_aggregate_full<float>, n), THREADS, 0, S(stream)>>>(
+            static_cast<const float*>(grads), nc, stride, n, out);
+    } else if (dt == CDSGD_F64) {
+        k_aggregate_full<double><<<flat_grid(k_aggregate_full<double>, n), THREADS, 0, S(stream)>>>(
+            static_cast<const double*>(grads), nc, stride, n, out);
+    } else {
+        return fail(CDSGD_ERR_ARG, "bad dtype");
+    }
+    LAUNCH_CHECK();
+    return CDSGD_OK;
+}
+
+extern "C" int cdsgd_pack_symbols(const uint8_t* sym, int64_t n, uint32_t* words, uint64_t* err, void* stream) {
+    if (n < 0) return fail(CDSGD_ERR_ARG, "n must be >= 0");
+    if (n == 0) return CDSGD_OK;
+    k_pack<<<flat_grid(k_pack, (n + 15) / 16), THREADS, 0, S(stream)>>>(sym, n, words, err);
+    LAUNCH_CHECK();
+    return CDSGD_OK;
+}
+
+extern "C" int cdsgd_unpack_symbols(const uint32_t* words, int64_t length, uint8_t* sym, void* stream) {
+    if (length < 0) return fail(CDSGD_ERR_ARG, "length must be >= 0");
+    if (length == 0) return CDSGD_OK;
+    k_unpack<<<flat_grid(k_unpack, length), THREADS, 0, S(stream)>>>(words, length, sym);
+    LAUNCH_CHECK();
+    return CDSGD_OK;
+}
+
+extern "C" int cdsgd_global_update(void* w, int32_t wdt, const void* mean, int32_t mdt, int64_t n, double eta,
+                                   void* stream) {
+    if (eta < 0) return fail(CDSGD_ERR_ARG, "eta_global must be >= 0");
+    if (n == 0) return CDSGD_OK;
+#define GU(TW, TM)                                                                               \
+    k_global_update<TW, TM><<<flat_grid(k_global_update<TW, TM>, n), THREADS, 0, S(stream)>>>(  \
+        static_cast<TW*>(w), static_cast<const TM*>(mean), n, eta)
+    if (wdt == CDSGD_F32 && mdt == CDSGD_F32) GU(float, float);
+    else if (wdt == CDSGD_F32 && mdt == CDSGD_F64) GU(float, double);
+    else if (wdt == CDSGD_F64 && mdt == CDSGD_F32) GU(double, float);
+    else if (wdt == CDSGD_F64 && mdt == CDSGD_F64) GU(double, double);
+    else return fail(CDSGD_ERR_ARG, "bad dtype");
+#undef GU
+    LAUNCH_CHECK();
+    return CDSGD_OK;
+}
+
+extern "C" int cdsgd_local_update(const void* base, int32_t bdt, const void* g, int32_t gdt, void* out,
+                                  int32_t odt, int64_t n, double eta_l, void* stream) {
+    if (eta_l < 0) return fail(CDSGD_ERR_ARG, "eta_local must be >= 0");
+    if (n == 0) return CDSGD_OK;
+    if (bdt < 0 || bdt > 1 || gdt < 0 || gdt > 1 || odt < 0 || odt > 1) return fail(CDSGD_ERR_ARG, "bad dtype");
+#define LU(TB, TG, TO)                                                                                   \
+    k_local_update<TB, TG, TO><<<flat_grid(k_local_update<TB, TG, TO>, n), THREADS, 0, S(stream)>>>(   \
+        static_cast<const TB*>(base), static_cast<const TG*>(g), static_cast<TO*>(out), n, eta_l)
+    const int code = bdt * 4 + gdt * 2 + odt;
+    switch (code) {
+        case 0: LU(float, float, float); break;
+        case 1: LU(float, float, double); break;
+        case 2: LU(float, double, float); break;
+        case 3: LU(float, double, double); break;
+        case 4: LU(double, float, float); break;
+        case 5: LU(double, float, double); break;
+        case 6: LU(double, double, float); break;
+        default: LU(double, double, double); break;
+    }
+#undef LU
+    LAUNCH_CHECK();
+    return CDSGD_OK;
+}
+
+// ------------------------------------------------------------------ fused apply
+namespace {
+// True if every partial sum j*alpha (|j| <= nr) is exactly representable, i.e. the
+// ascending fp64 sum of nr decoded values equals cnt*alpha in any order.
+bool alpha_exact(double alpha, int nr) {
+    for (int j = 1; j <= nr; ++j) {
+        const double v = static_cast<double>(j) * alpha;
+        if (static_cast<long double>(v) != static_cast<long double>(j) * static_cast<long double>(alpha)) return false;
+        if (!std::isfinite(v)) return false;
+    }
+    return true;
+}
+void build_tab(DecodeTab& tab, double alpha, double eta_g, int nr) {
+    memset(&tab, 0, sizeof(tab));
+    for (int c = -nr; c <= nr; ++c) {
+        const double total = static_cast<double>(c) * alpha;          // exact (alpha_exact)
+        const double mean = total / static_cast<double>(nr);          // engine.py:255
+        tab.mean[c + nr] = mean;
+        tab.upd[c + nr] = static_cast<float>(eta_g * mean);           // engine.py:511 (eta*mean)
+    }
+}
+inline bool pow2(int n) { return n > 0 && (n & (n - 1)) == 0; }
+
+int launch_apply_quant(const cdsgd_layout* L, float* W, const uint32_t* gathered, int nr, int64_t stride,
+                       double alpha, double eta_g, const float* gnext, float* loc, double eta_l, uint64_t* err,
+                       uint64_t skip_below, double* gnorm, const DecodeTab* tab_in, int exact_in,
+                       cudaStream_t st) {
+    if (L == nullptr) return fail(CDSGD_ERR_ARG, "layout is NULL");
+    if (nr < 1 || nr > MAX_RANKS - 1) return fail(CDSGD_ERR_ARG, "nranks must be in [1, %d]", MAX_RANKS - 1);
+    if ((gnext == nullptr) != (loc == nullptr)) return fail(CDSGD_ERR_ARG, "g_next and loc_out go together");
+    if (L->n == 0) return CDSGD_OK;
+    ApplyQArgs a;
+    a.W = W;
+    a.gathered = gathered;
+    a.stride = stride;
+    a.gnext = gnext;
+    a.loc = loc;
+    a.alpha = alpha;
+    a.inv_n_or_zero = pow2(nr) ? 1.0 / nr : 0.0;
+    a.eta_g_d = eta_g;
+    a.eta_l_d = eta_l;
+    a.eta_l = static_cast<float>(eta_l);
+    a.nranks = nr;
+    a.err = err;
+    a.skip_below = skip_below;
+    a.gnorm = gnorm;
+    DecodeTab tab;
+    int exact;
+    if (tab_in != nullptr) {
+        tab = *tab_in;
+        exact = exact_in;
+    } else {
+        exact = alpha_exact(alpha, nr) ? 1 : 0;
+        build_tab(tab, alpha, eta_g, nr);
+    }
+    a.exact = exact;
+    const KeyTab kt = L->tab();
+#define AQ(R)                                                                                   \
+    case R:                                                                                     \
+        k_apply_quant<R><<<tile_grid(k_apply_quant<R>, kt.ntiles), THREADS, 0, st>>>(a, kt, tab); \
+        break
+    switch (nr) {
+        AQ(1); AQ(2); AQ(3); AQ(4); AQ(5); AQ(6); AQ(7); AQ(8);
+        default:
+            k_apply_quant<0><<<tile_grid(k_apply_quant<0>, kt.ntiles), THREADS, 0, st>>>(a, kt, tab);
+    }
+#undef AQ
+    LAUNCH_CHECK();
+    return CDSGD_OK;
+}
+
+int launch_apply_full(float* W, const float* gsum, int nr, int64_t n, double eta_g, const float* gnext,
+                      float* loc, double eta_l, const uint64_t* err, uint64_t skip_below, double* gnorm,
+                      cudaStream_t st) {
+    if (nr < 1) return fail(CDSGD_ERR_ARG, "nranks must be >= 1");
+    if ((gnext == nullptr) != (loc == nullptr)) return fail(CDSGD_ERR_ARG, "g_next and loc_out go together");
+    if (n == 0) return CDSGD_OK;
+    ApplyFArgs a;
+    a.W = W;
+    a.gsum = gsum;
+    a.gnext = gnext;
+    a.loc = loc;
+    a.scale = static_cast<float>(eta_g / nr);
+    a.eta_l = static_cast<float>(eta_l);
+    a.inv_n = 1.0 / nr;
+    a.n = n;
+    a.err = err;
+    a.skip_below = skip_below;
+    a.gnorm = gnorm;
+    k_apply_full<<<flat_grid(k_apply_full, (n + 7) / 8), THREADS, 0, st>>>(a);
+    LAUNCH_CHECK();
+    return CDSGD_OK;
+}
+}  // namespace
+
+extern "C" int cdsgd_apply_quant(const cdsgd_layout* L, float* W, const uint32_t* gathered, int32_t nr,
+                                 int64_t stride, double alpha, double eta_g, const float* gnext, float* loc,
+                                 double eta_l, uint64_t* err, uint64_t skip_below, double* gnorm, void* stream) {
+    if (!(alpha > 0.0)) return fail(CDSGD_ERR_ARG, "threshold alpha must be > 0");
+    return launch_apply_quant(L, W, gathered, nr, stride, alpha, eta_g, gnext, loc, eta_l, err, skip_below, gnorm,
+                              nullptr, 0, S(stream));
+}
+
+extern "C" int cdsgd_apply_full(float* W, const float* gsum, int32_t nr, int64_t n, double eta_g,
+                                const float* gnext, float* loc, double eta_l, const uint64_t* err,
+                                uint64_t skip_below, double* gnorm, void* stream) {
+    return launch_apply_full(W, gsum, nr, n, eta_g, gnext, loc, eta_l, err, skip_below, gnorm, S(stream));
+}
+
+// ------------------------------------------------------------------ NCCL exchange
+struct cdsgd_comm {
+    ncclComm_t nccl = nullptr;
+    int nranks = 1, rank = 0;
+};
+
+extern "C" int cdsgd_comm_unique_id(void* out) {
+    static_assert(sizeof(ncclUniqueId) == CDSGD_UNIQUE_ID_BYTES, "ncclUniqueId size");
+    if (out == nullptr) return fail(CDSGD_ERR_ARG, "out is NULL");
+    ncclUniqueId id;
+    NCCL_TRY(ncclGetUniqueId(&id));
+    memcpy(out, &id, sizeof(id));
+    return CDSGD_OK;
+}
+
+extern "C" int cdsgd_comm_init(const void* uid, int32_t nranks, int32_t rank, cdsgd_comm** out) {
+    if (out == nullptr || uid == nullptr) return fail(CDSGD_ERR_ARG, "NULL argument");
+    if (nranks < 1 || rank < 0 || rank >= nranks) return fail(CDSGD_ERR_ARG, "bad rank %d of %d", rank, nranks);
+    ncclUniqueId id;
+    memcpy(&id, uid, sizeof(id));
+    cdsgd_comm* c = new cdsgd_comm();
+    c->nranks = nranks;
+    c->rank = rank;
+    ncclResult_t r = ncclCommInitRank(&c->nccl, nranks, id, rank);
+    if (r != ncclSuccess) {
+        delete c;
+        return fail(CDSGD_ERR_NCCL, "ncclCommInitRank: %s", ncclGetErrorString(r));
+    }
+    *out = c;
+    return CDSGD_OK;
+}
+
+extern "C" int cdsgd_comm_destroy(cdsgd_comm* c) {
+    if (c == nullptr) return CDSGD_OK;
+    if (c->nccl) ncclCommDestroy(c->nccl);
+    delete c;
+    return CDSGD_OK;
+}
+
+extern "C" int cdsgd_allgather_words(cdsgd_comm* c, const uint32_t* send, uint32_t* recv, int64_t words,
+                                     void* stream) {
+    if (c == nullptr) return fail(CDSGD_ERR_ARG, "comm is NULL");
+    NCCL_TRY(ncclAllGather(send, recv, static_cast<size_t>(words), ncclUint32, c->nccl, S(stream)));
+    return CDSGD_OK;
+}
+
+extern "C" int cdsgd_allreduce_sum_f32(cdsgd_comm* c, const float* send, float* recv, int64_t n, void* stream) {
+    if (c == nullptr) return fail(CDSGD_ERR_ARG, "comm is NULL");
+    NCCL_TRY(ncclAllReduce(send, recv, static_cast<size_t>(n), ncclFloat, ncclSum, c->nccl, S(stream)));
+    return CDSGD_OK;
+}
+
+// ------------------------------------------------------------------ step engine
+struct cdsgd_engine {
+    cdsgd_engine_desc d{};
+    const cdsgd_layout* L = nullptr;
+    cdsgd_comm* comm = nullptr;
+    cudaStream_t xs = nullptr;
+    cudaEvent_t evQ[2] = {nullptr, nullptr};
+    cudaEvent_t evX[2] = {nullptr, nullptr};
+    DecodeTab tab{};
+    int exact = 0;
+    bool uses_local = false;
+    int64_t n_warmup = 0;
+    // state
+    int64_t t = 0;
+    int rcur = 0;
+    bool compute_is_loc = false;
+    bool pending = false;
+    int64_t pend_t = 0;
+    bool pend_comp = false;
+    const float* pend_grad = nullptr;
+    bool failed = false;
+    int64_t err_base = 0;
+    std::vector<int8_t> rlog;  // residual index at the entry of rounds err_base..t-1
+    // profiling: event pairs per kernel class (0 quant, 1 apply_q, 2 apply_f, 3 local, 4 exchange)
+    bool prof = false;
+    std::vector<cudaEvent_t> ev_pool;
+    size_t ev_used = 0;
+    std::vector<std::pair<int, size_t>> prof_marks;  // (class, index of start event)
+};
+
+namespace {
+// Records a start event on `st` and returns its pool index (or -1 when not profiling).
+long prof_start(cdsgd_engine* E, int cls, cudaStream_t st) {
+    if (!E->prof) return -1;
+    while (E->ev_pool.size() < E->ev_used + 2) {
+        cudaEvent_t ev;
+        if (cudaEventCreate(&ev) != cudaSuccess) return -1;
+        E->ev_pool.push_back(ev);
+    }
+    const size_t i = E->ev_used;
+    E->ev_used += 2;
+    cudaEventRecord(E->ev_pool[i], st);
+    E->prof_marks.emplace_back(cls, i);
+    return static_cast<long>(i);
+}
+void prof_stop(cdsgd_engine* E, long i, cudaStream_t st) {
+    if (i >= 0) cudaEventRecord(E->ev_pool[i + 1], st);
+}
+
+// Worker._push_compressed (engine.py:345-355) + should_compress (engine.py:217-223).
+int round_compressed(const cdsgd_engine* E, int64_t t, bool* out) {
+    const bool in_warm = E->uses_local && t < E->n_warmup;
+    if (in_warm) { *out = false; return CDSGD_OK; }
+    if (E->d.algo == CDSGD_ALGO_BITSGD) { *out = true; return CDSGD_OK; }
+    if (E->d.algo == CDSGD_ALGO_CDSGD) {
+        if (E->d.force_compress) { *out = true; return CDSGD_OK; }
+        const int64_t count = t - E->n_warmup + 1;
+        if (count < 1) return fail(CDSGD_ERR_ARG, "count must be >= 1 (engine.py:221-222)");
+        *out = (count % E->d.k) != 0;
+        return CDSGD_OK;
+    }
+    *out = false;
+    return CDSGD_OK;
+}
+
+int64_t words_of(const cdsgd_engine* E) { return E->L->nwords; }
+
+// Finish round p: wait for its exchange, then K2 (codes) or K3 (full) fused with
+// the local update from g_next (nullable).
+int engine_apply(cdsgd_engine* E, int64_t p, bool comp, const float* gp, const float* gnext, cudaStream_t C) {
+    const int nr = E->d.nranks;
+    if (nr > 1) CUDA_TRY(cudaStreamWaitEvent(C, E->evX[p & 1], 0));
+    const int64_t rel = p - E->err_base + 1;
+    const uint64_t skip_below = rel <= 0 ? 0ull : (static_cast<uint64_t>(rel) << CDSGD_INDEX_BITS);
+    double* gn = nullptr;
+    if (E->d.gnorm_sq != nullptr && E->d.gnorm_ring > 0) {
+        gn = E->d.gnorm_sq + (p % E->d.gnorm_ring);
+        CUDA_TRY(cudaMemsetAsync(gn, 0, sizeof(double), C));
+    }
+    float* loc = gnext ? E->d.loc : nullptr;
+    if (comp) {
+        const long pi = prof_start(E, 1, C);
+        const int rc = launch_apply_quant(E->L, E->d.weights, E->d.gathered[p & 1], nr, words_of(E), E->d.alpha,
+                                          E->d.eta_global, gnext, loc, E->d.eta_local, E->d.err, skip_below, gn,
+                                          &E->tab, E->exact, C);
+        prof_stop(E, pi, C);
+        return rc;
+    }
+    const float* gsum = nr > 1 ? E->d.gsum[p & 1] : gp;
+    const long pi = prof_start(E, 2, C);
+    const int rc = launch_apply_full(E->d.weights, gsum, nr, E->L->n, E->d.eta_global, gnext, loc, E->d.eta_local,
+                                     E->d.err, skip_below, gn, C);
+    prof_stop(E, pi, C);
+    return rc;
+}
+}  // namespace
+
+extern "C" int cdsgd_engine_create(const cdsgd_engine_desc* d, const cdsgd_layout* L, cdsgd_comm* comm,
+                                   cdsgd_engine** out) {
+    if (out == nullptr || d == nullptr || L == nullptr) return fail(CDSGD_ERR_ARG, "NULL argument");
+    *out = nullptr;
+    if (d->algo < CDSGD_ALGO_SSGD || d->algo > CDSGD_ALGO_CDSGD) return fail(CDSGD_ERR_ARG, "unknown algo %d", d->algo);
+    if (d->nranks < 1 || d->nranks > MAX_RANKS - 1) return fail(CDSGD_ERR_ARG, "workers must be in [1, %d]", MAX_RANKS - 1);
+    if (d->rank < 0 || d->rank >= d->nranks) return fail(CDSGD_ERR_ARG, "rank out of range");
+    if (d->k < 1) return fail(CDSGD_ERR_ARG, "k must be >= 1");
+    if (d->warmup_n < 0) return fail(CDSGD_ERR_ARG, "warmup_n must be >= 0");
+    if (!(d->alpha > 0.0)) return fail(CDSGD_ERR_ARG, "alpha must be > 0");
+    if (!(d->eta_global > 0.0) || !(d->eta_local > 0.0)) return fail(CDSGD_ERR_ARG, "learning rates must be > 0");
+    if (!d->weights || !d->loc || !d->residual[0] || !d->residual[1] || !d->gathered[0] || !d->gathered[1] || !d->err)
+        return fail(CDSGD_ERR_ARG, "NULL engine buffer");
+    if (d->nranks > 1 && (comm == nullptr || !d->gsum[0] || !d->gsum[1]))
+        return fail(CDSGD_ERR_ARG, "nranks > 1 needs a comm and gsum buffers");
+    if (comm != nullptr && (comm->nranks != d->nranks || comm->rank != d->rank))
+        return fail(CDSGD_ERR_ARG, "comm rank/size mismatch");
+    cdsgd_engine* E = new cdsgd_engine();
+    E->d = *d;
+    E->L = L;
+    E->comm = comm;
+    E->uses_local = (d->algo == CDSGD_ALGO_LUSGD || d->algo == CDSGD_ALGO_CDSGD) && !d->bypass_local;
+    E->n_warmup = (d->algo == CDSGD_ALGO_LUSGD || d->algo == CDSGD_ALGO_CDSGD) ? d->warmup_n : 0;
+    E->exact = alpha_exact(d->alpha, d->nranks) ? 1 : 0;
+    build_tab(E->tab, d->alpha, d->eta_global, d->nranks);
+    E->compute_is_loc = E->uses_local && E->n_warmup == 0;
+    cudaError_t e = cudaSuccess;
+    if (d->nranks > 1) {
+        int lo = 0, hi = 0;
+        cudaDeviceGetStreamPriorityRange(&lo, &hi);
+        e = cudaStreamCreateWithPriority(&E->xs, cudaStreamNonBlocking, hi);
+        for (int i = 0; i < 2 && e == cudaSuccess; ++i) {
+            e = cudaEventCreateWithFlags(&E->evQ[i], cudaEventDisableTiming);
+            if (e == cudaSuccess) e = cudaEventCreateWithFlags(&E->evX[i], cudaEventDisableTiming);
+        }
+    }
+    if (e != cudaSuccess) {
+        cdsgd_engine_destroy(E);
+        return fail(CDSGD_ERR_CUDA, "engine streams/events: %s", cudaGetErrorString(e));
+    }
+    *out = E;
+    return CDSGD_OK;
+}
+
+extern "C" int cdsgd_engine_join(cdsgd_engine* E, void* stream) {
+    if (E == nullptr) return fail(CDSGD_ERR_ARG, "NULL engine");
+    if (E->xs == nullptr || E->t == 0) return CDSGD_OK;
+    CUDA_TRY(cudaStreamWaitEvent(S(stream), E->evX[(E->t - 1) & 1], 0));
+    return CDSGD_OK;
+}
+
+extern "C" int cdsgd_engine_profile_begin(cdsgd_engine* E) {
+    if (E == nullptr) return fail(CDSGD_ERR_ARG, "NULL engine");
+    E->prof = true;
+    E->ev_used = 0;
+    E->prof_marks.clear();
+    return CDSGD_OK;
+}
+
+extern "C" int cdsgd_engine_profile_end(cdsgd_engine* E, double* out) {
+    if (E == nullptr || out == nullptr) return fail(CDSGD_ERR_ARG, "NULL argument");
+    E->prof = false;
+    for (int i = 0; i < 10; ++i) out[i] = 0.0;
+    for (const auto& m : E->prof_marks) {
+        CUDA_TRY(cudaEventSynchronize(E->ev_pool[m.second + 1]));
+        float ms = 0.f;
+        CUDA_TRY(cudaEventElapsedTime(&ms, E->ev_pool[m.second], E->ev_pool[m.second + 1]));
+        out[2 * m.first] += ms;
+        out[2 * m.first + 1] += 1.0;
+    }
+    E->prof_marks.clear();
+    E->ev_used = 0;
+    return CDSGD_OK;
+}
+
+extern "C" int cdsgd_engine_destroy(cdsgd_engine* E) {
+    if (E == nullptr) return CDSGD_OK;
+    if (E->xs) cudaStreamSynchronize(E->xs);
+    for (cudaEvent_t ev : E->ev_pool) cudaEventDestroy(ev);
+    for (int i = 0; i < 2; ++i) {
+        if (E->evQ[i]) cudaEventDestroy(E->evQ[i]);
+        if (E->evX[i]) cudaEventDestroy(E->evX[i]);
+    }
+    if (E->xs) cudaStreamDestroy(E->xs);
+    delete E;
+    return CDSGD_OK;
+}
+
+extern "C" int cdsgd_engine_round_compressed(const cdsgd_engine* E, int64_t t) {
+    bool c = false;
+    if (E == nullptr || round_compressed(E, t, &c) != CDSGD_OK) return -1;
+    return c ? 1 : 0;
+}
+
+extern "C" int cdsgd_engine_step(cdsgd_engine* E, const float* g, void* stream) {
+    if (E == nullptr || g == nullptr) return fail(CDSGD_ERR_ARG, "NULL argument");
+    if (E->failed) return fail(CDSGD_ERR_STATE, "engine failed at an earlier round; see cdsgd_engine_check");
+    if (E->t - E->err_base >= (int64_t(1) << 23))
+        return fail(CDSGD_ERR_STATE, "cdsgd_engine_check must run at least every 2^23 rounds");
+    cudaStream_t C = S(stream);
+    const int64_t t = E->t;
+    bool comp = false;
+    int rc = round_compressed(E, t, &comp);
+    if (rc != CDSGD_OK) return rc;
+    const int nr = E->d.nranks;
+    const int64_t nw = words_of(E);
+    uint32_t* mine = E->d.gathered[t & 1] + static_cast<int64_t>(E->d.rank) * nw;
+    // 1. this round's contribution (K1 on compressed rounds)
+    E->rlog.push_back(static_cast<int8_t>(E->rcur));
+    if (comp) {
+        const uint64_t tag = static_cast<uint64_t>(t - E->err_base) << CDSGD_INDEX_BITS;
+        const long pi = prof_start(E, 0, C);
+        rc = cdsgd_quantize(E->L, g, CDSGD_F32, E->d.residual[E->rcur], E->d.residual[E->rcur ^ 1], mine,
+                            E->d.alpha, E->d.err, tag, C);
+        prof_stop(E, pi, C);
+        if (rc != CDSGD_OK) return rc;
+        E->rcur ^= 1;
+    }
+    // 2. exchange round t on the engine's stream
+    if (nr > 1) {
+        CUDA_TRY(cudaEventRecord(E->evQ[t & 1], C));
+        CUDA_TRY(cudaStreamWaitEvent(E->xs, E->evQ[t & 1], 0));
+        const long pi = prof_start(E, 4, E->xs);
+        if (comp) {
+            NCCL_TRY(ncclAllGather(mine, E->d.gathered[t & 1], static_cast<size_t>(nw), ncclUint32, E->comm->nccl, E->xs));
+        } else {
+            NCCL_TRY(ncclAllReduce(g, E->d.gsum[t & 1], static_cast<size_t>(E->L->n), ncclFloat, ncclSum,
+                                   E->comm->nccl, E->xs));
+        }
+        prof_stop(E, pi, E->xs);
+        CUDA_TRY(cudaEventRecord(E->evX[t & 1], E->xs));
+    }
+    // 3. apply
+    const bool sync_path = !E->uses_local || t < E->n_warmup - 1;
+    if (sync_path) {
+        if (E->pending) return fail(CDSGD_ERR_STATE, "internal: pending round on the synchronous path");
+        rc = engine_apply(E, t, comp, g, nullptr, C);
+        if (rc != CDSGD_OK) return rc;
+        E->compute_is_loc = false;
+    } else {
+        if (E->pending) {
+            rc = engine_apply(E, E->pend_t, E->pend_comp, E->pend_grad, g, C);
+        } else {
+            // first local round: loc_{t+1} = W_t - eta_l * g_t (engine.py:380-382, 385-391)
+            const long pi = prof_start(E, 3, C);
+            rc = cdsgd_local_update(E->d.weights, CDSGD_F32, g, CDSGD_F32, E->d.loc, CDSGD_F32, E->L->n,
+                                    E->d.eta_local, stream);
+            prof_stop(E, pi, C);
+        }
+        if (rc != CDSGD_OK) return rc;
+        E->pending = true;
+        E->pend_t = t;
+        E->pend_comp = comp;
+        E->pend_grad = g;
+        E->compute_is_loc = true;
+    }
+    E->t = t + 1;
+    return CDSGD_OK;
+}
+
+extern "C" int cdsgd_engine_flush(cdsgd_engine* E, void* stream) {
+    if (E == nullptr) return fail(CDSGD_ERR_ARG, "NULL engine");
+    if (!E->pending) return CDSGD_OK;
+    const int rc = engine_apply(E, E->pend_t, E->pend_comp, E->pend_grad, nullptr, S(stream));
+    if (rc != CDSGD_OK) return rc;
+    E->pending = false;
+    E->pend_grad = nullptr;
+    // The next round computes at the now-current global weights' local step;
+    // loc already holds W_{t-1} - eta_l*g_{t-1}, which is what round t reads.
+    return CDSGD_OK;
+}
+
+extern "C" int cdsgd_engine_get_state(const cdsgd_engine* E, cdsgd_engine_state* out) {
+    if (E == nullptr || out == nullptr) return fail(CDSGD_ERR_ARG, "NULL argument");
+    out->t = E->t;
+    out->residual_index = E->rcur;
+    out->compute_is_loc = E->compute_is_loc ? 1 : 0;
+    out->pending = E->pending ? 1 : 0;
+    out->last_compressed = E->pend_comp ? 1 : 0;
+    out->failed = E->failed ? 1 : 0;
+    return CDSGD_OK;
+}
+
+extern "C" int cdsgd_engine_check(cdsgd_engine* E, void* stream, int64_t* round, int64_t* index) {
+    if (E == nullptr) return fail(CDSGD_ERR_ARG, "NULL engine");
+    CUDA_TRY(cudaStreamSynchronize(S(stream)));
+    if (E->xs) CUDA_TRY(cudaStreamSynchronize(E->xs));
+    if (E->comm != nullptr) {
+        ncclResult_t ar = ncclSuccess;
+        NCCL_TRY(ncclCommGetAsyncError(E->comm->nccl, &ar));
+        if (ar != ncclSuccess) return fail(CDSGD_ERR_NCCL, "NCCL async error: %s", ncclGetErrorString(ar));
+    }
+    uint64_t h[2];
+    CUDA_TRY(cudaMemcpy(h, E->d.err, sizeof(h), cudaMemcpyDeviceToHost));
+    if (h[0] != NO_ERR) {
+        const int64_t rel = static_cast<int64_t>(h[0] >> CDSGD_INDEX_BITS);
+        const int64_t idx = static_cast<int64_t>(h[0] & ((uint64_t(1) << CDSGD_INDEX_BITS) - 1));
+        const int64_t s = E->err_base + rel;
+        if (round) *round = s;
+        if (index) *index = idx;
+        if (rel >= 0 && rel < static_cast<int64_t>(E->rlog.size())) E->rcur = E->rlog[rel];
+        E->failed = true;
+        return fail(CDSGD_ERR_NUMERIC, "non-finite accumulated gradient at round %lld, element %lld",
+                    (long long)s, (long long)idx);
+    }
+    if (h[1] != NO_ERR) {
+        if (index) *index = static_cast<int64_t>(h[1]);
+        E->failed = true;
+        return fail(CDSGD_ERR_CORRUPT, "reserved symbol 11 at element %lld", (long long)h[1]);
+    }
+    E->err_base = E->t;
+    E->rlog.clear();
+    return CDSGD_OK;
+}

@@ -1,0 +1,637 @@
+// kernels.cuh — sm_100a device code of the CD-SGD hot path.
+//
+// Data layout in HBM (one rank):
+//   g        fp32[n]          this round's gradient (caller-owned)
+//   r[2]     fp64[n]          ping-pong error-feedback residual (exact mode)
+//   words    u32[W(n)]        2-bit codes, 16 per word, packing restarts per key
+//   W, loc   fp32[n]          replicated global weights / local compute weights
+//
+// Work unit: a "tile" = up to 32 packed words (512 elements) of ONE key. Tiles
+// never straddle keys (per-key packing restart, codec.py:147-148 via
+// engine.py:397-402), so only the last tile of a key can be partial. Each warp
+// owns a contiguous range of tiles (grid = resident warps), walks keys
+// incrementally and, for full 32B-aligned tiles, moves data with 128-bit
+// (fp32) and 256-bit (fp64) vector loads/stores: lane l owns elements
+// [128c + 4l, 128c + 4l + 4) of chunk c (c = 0..3), so every warp-wide access
+// is fully coalesced. Codes are packed with two xor-shuffles (4 lanes -> one
+// word) and one index shuffle so lane j stores word j (one 128 B store).
+// Partial / misaligned tiles take a coalesced scalar path that packs with
+// __ballot_sync (lane l owns element 32s + l) and a Morton bit interleave.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace cdsgd {
+
+constexpr unsigned FULL = 0xffffffffu;
+constexpr int TILE_WORDS = 32;
+constexpr int TILE_ELEMS = 512;
+constexpr int CHUNKS = 4;           // 128-element chunks per tile (fast path)
+constexpr uint64_t NO_ERR = ~0ull;
+
+struct KeyTab {
+    const int64_t* eoff;  // [nkeys+1] element offsets
+    const int64_t* woff;  // [nkeys+1] word offsets
+    const int64_t* toff;  // [nkeys+1] tile offsets
+    int32_t nkeys;
+    int64_t ntiles;
+};
+
+// ---------------------------------------------------------------- memory helpers
+__device__ __forceinline__ float4 ld_stream(const float* p) {
+    float4 v;
+    asm("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+        : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
+    return v;
+}
+struct d4 { double x, y, z, w; };
+__device__ __forceinline__ d4 ld_stream(const double* p) {
+    d4 v;
+    asm("ld.global.nc.L1::no_allocate.v4.f64 {%0,%1,%2,%3}, [%4];"
+        : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ void st_stream(double* p, double a, double b, double c, double d) {
+    asm volatile("st.global.L1::no_allocate.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(a), "d"(b),
+                 "d"(c), "d"(d));
+}
+__device__ __forceinline__ void st_stream(float* p, float a, float b, float c, float d) {
+    asm volatile("st.global.L1::no_allocate.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(a), "f"(b),
+                 "f"(c), "f"(d));
+}
+__device__ __forceinline__ uint32_t ld_word(const uint32_t* p) {
+    uint32_t v;
+    asm("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(v) : "l"(p));
+    return v;
+}
+
+template <typename G> struct GVec;
+template <> struct GVec<float> {
+    float v[4];
+    __device__ __forceinline__ void load(const float* p) {
+        float4 t = ld_stream(p);
+        v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w;
+    }
+};
+template <> struct GVec<double> {
+    double v[4];
+    __device__ __forceinline__ void load(const double* p) {
+        d4 t = ld_stream(p);
+        v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w;
+    }
+};
+
+__device__ __forceinline__ bool aligned_to(const void* p, uintptr_t a) {
+    return (reinterpret_cast<uintptr_t>(p) & (a - 1)) == 0;
+}
+
+// 16 low bits of x spread to the even bit positions of a 32-bit word.
+__device__ __forceinline__ uint32_t spread16(uint32_t x) {
+    x &= 0xffffu;
+    x = (x | (x << 8)) & 0x00ff00ffu;
+    x = (x | (x << 4)) & 0x0f0f0f0fu;
+    x = (x | (x << 2)) & 0x33333333u;
+    x = (x | (x << 1)) & 0x55555555u;
+    return x;
+}
+// Word of 16 two-bit codes from plus/minus lane masks (bit i = element i).
+__device__ __forceinline__ uint32_t interleave_codes(uint32_t plus16, uint32_t minus16) {
+    return spread16(plus16) | (spread16(minus16) << 1);
+}
+
+__device__ __forceinline__ bool nonfinite(double a) {
+    return (static_cast<uint32_t>(__double2hiint(a)) & 0x7ff00000u) == 0x7ff00000u;
+}
+
+// ---------------------------------------------------------------- tile walking
+// Warp `wid` of `nwarps` owns tiles [t_begin, t_end). The key containing a tile
+// is found once by binary search, then advanced incrementally.
+struct TileCursor {
+    int k;
+    int64_t t0, t1;  // tile range of key k
+    int64_t e0, e1;  // element range of key k
+    int64_t w0, w1;  // word range of key k
+    __device__ __forceinline__ void load(const KeyTab& kt, int key) {
+        k = key;
+        t0 = __ldg(kt.toff + k); t1 = __ldg(kt.toff + k + 1);
+        e0 = __ldg(kt.eoff + k); e1 = __ldg(kt.eoff + k + 1);
+        w0 = __ldg(kt.woff + k); w1 = __ldg(kt.woff + k + 1);
+    }
+    __device__ __forceinline__ void seek(const KeyTab& kt, int64_t tile) {
+        int lo = 0, hi = kt.nkeys - 1;
+        while (lo < hi) {
+            int mid = (lo + hi + 1) >> 1;
+            if (__ldg(kt.toff + mid) <= tile) lo = mid; else hi = mid - 1;
+        }
+        load(kt, lo);
+    }
+    __device__ __forceinline__ void advance_to(const KeyTab& kt, int64_t tile) {
+        while (tile >= t1) load(kt, k + 1);
+    }
+};
+
+__device__ __forceinline__ void warp_range(int64_t ntiles, int64_t& b, int64_t& e) {
+    const int64_t wid = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+    const int64_t per = (ntiles + nw - 1) / nw;
+    b = wid * per;
+    e = b + per < ntiles ? b + per : ntiles;
+}
+
+__device__ __forceinline__ uint64_t warp_min_u64(uint64_t v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        uint64_t u = __shfl_xor_sync(FULL, v, o);
+        v = u < v ? u : v;
+    }
+    return v;
+}
+
+// ================================================================ K1: quantize
+// codec.quantize (codec.py:164-194) per key, fp64 exact:
+//   acc = r + (double)g; plus = acc >= a; minus = acc <= -a;
+//   r' = acc - (plus ? a : minus ? -a : 0.0); code 01/10/00.
+template <typename G>
+__device__ __forceinline__ uint32_t quant1(double r, G g, double alpha, double& rn, bool& bad) {
+    const double acc = __dadd_rn(r, static_cast<double>(g));
+    bad = nonfinite(acc);
+    const bool p = acc >= alpha;
+    const bool m = acc <= -alpha;
+    const double em = p ? alpha : (m ? -alpha : 0.0);
+    rn = __dsub_rn(acc, em);
+    return p ? 1u : (m ? 2u : 0u);
+}
+
+template <typename G>
+__global__ void __launch_bounds__(256) k_quantize(const G* __restrict__ g, const double* r_in,
+                                                  double* r_out, uint32_t* __restrict__ words,
+                                                  KeyTab kt, double alpha, uint64_t* err,
+                                                  uint64_t tag) {
+    if (err != nullptr && *reinterpret_cast<volatile uint64_t*>(err) != NO_ERR) return;
+    int64_t tb, te;
+    warp_range(kt.ntiles, tb, te);
+    if (tb >= te) return;
+    const int lane = threadIdx.x & 31;
+    TileCursor kc;
+    kc.seek(kt, tb);
+    uint64_t bad_idx = NO_ERR;
+    for (int64_t ti = tb; ti < te; ++ti) {
+        kc.advance_to(kt, ti);
+        const int64_t j = ti - kc.t0;
+        const int64_t e0 = kc.e0 + j * TILE_ELEMS;
+        const int64_t w0 = kc.w0 + j * TILE_WORDS;
+        const int64_t ne64 = kc.e1 - e0;
+        const int ne = ne64 < TILE_ELEMS ? static_cast<int>(ne64) : TILE_ELEMS;
+        const int64_t nw64 = kc.w1 - w0;
+        const int nw = nw64 < TILE_WORDS ? static_cast<int>(nw64) : TILE_WORDS;
+        const bool fast = ne == TILE_ELEMS && aligned_to(g + e0, 4 * sizeof(G)) &&
+                          aligned_to(r_in + e0, 32) && aligned_to(r_out + e0, 32);
+        uint32_t myword = 0;
+        if (fast) {
+            GVec<G> gv[CHUNKS];
+            d4 rv[CHUNKS];
+#pragma unroll
+            for (int c = 0; c < CHUNKS; ++c) {
+                const int64_t e = e0 + 128 * c + 4 * lane;
+                gv[c].load(g + e);
+                rv[c] = ld_stream(r_in + e);
+            }
+#pragma unroll
+            for (int c = 0; c < CHUNKS; ++c) {
+                const int64_t e = e0 + 128 * c + 4 * lane;
+                double o0, o1, o2, o3;
+                bool b0, b1, b2, b3;
+                uint32_t code = quant1(rv[c].x, gv[c].v[0], alpha, o0, b0);
+                code |= quant1(rv[c].y, gv[c].v[1], alpha, o1, b1) << 2;
+                code |= quant1(rv[c].z, gv[c].v[2], alpha, o2, b2) << 4;
+                code |= quant1(rv[c].w, gv[c].v[3], alpha, o3, b3) << 6;
+                st_stream(r_out + e, o0, o1, o2, o3);
+                if (b0 | b1 | b2 | b3) {
+                    const int first = b0 ? 0 : b1 ? 1 : b2 ? 2 : 3;
+                    const uint64_t idx = tag | static_cast<uint64_t>(e + first);
+                    bad_idx = idx < bad_idx ? idx : bad_idx;
+                }
+                // 4 lanes x 8 bits -> word (8c + lane/4) of this tile
+                uint32_t v = code << (8 * (lane & 3));
+                v |= __shfl_xor_sync(FULL, v, 1);
+                v |= __shfl_xor_sync(FULL, v, 2);
+                const uint32_t s = __shfl_sync(FULL, v, 4 * (lane & 7));
+                if ((lane >> 3) == c) myword = s;
+            }
+        } else {
+#pragma unroll 4
+            for (int s = 0; s < TILE_ELEMS / 32; ++s) {
+                const int el = 32 * s + lane;
+                const bool valid = el < ne;
+                bool p = false, m = false;
+                if (valid) {
+                    double o;
+                    bool b;
+                    const uint32_t code = quant1(r_in[e0 + el], g[e0 + el], alpha, o, b);
+                    r_out[e0 + el] = o;
+                    p = code == 1u;
+                    m = code == 2u;
+                    if (b) {
+                        const uint64_t idx = tag | static_cast<uint64_t>(e0 + el);
+                        bad_idx = idx < bad_idx ? idx : bad_idx;
+                    }
+                }
+                const uint32_t pm = __ballot_sync(FULL, p);
+                const uint32_t mm = __ballot_sync(FULL, m);
+                if (lane == 2 * s) myword = interleave_codes(pm, mm);
+                if (lane == 2 * s + 1) myword = interleave_codes(pm >> 16, mm >> 16);
+            }
+        }
+        if (lane < nw) words[w0 + lane] = myword;
+    }
+    if (err != nullptr) {
+        bad_idx = warp_min_u64(bad_idx);
+        if (lane == 0 && bad_idx != NO_ERR) atomicMin(reinterpret_cast<unsigned long long*>(err),
+                                                      static_cast<unsigned long long>(bad_idx));
+    }
+}
+
+// ================================================================ decode helpers
+// Exact-alpha mode (the usual alpha = 0.5): every partial sum j*alpha, |j| <= N,
+// is representable, so the ascending-worker fp64 sum of engine.py:250-253 equals
+// cnt*alpha for cnt = #plus - #minus regardless of order. The host precomputes,
+// in fp64 exactly as the reference does, tab[cnt + N] = (cnt*alpha)/N and the
+// rounded fp32 update eta_g*mean; the kernel only counts codes (SWAR over
+// 4-bit fields: even elements at bits 4i, odd at 4i+2 before the shift).
+constexpr int MAX_RANKS = 16;
+struct DecodeTab {
+    double mean[2 * MAX_RANKS + 1];  // (cnt*alpha)/N
+    float upd[2 * MAX_RANKS + 1];    // (float)(eta_g * mean)
+};
+
+// Counts over ranks for the 16 codes of one word position: returns packed 4-bit
+// plus/minus counters for even (field 4i) and odd (field 4i) elements, and a
+// reserved-symbol mask (bit 2i set if code i of some rank is 11).
+struct Counts {
+    uint32_t pe, po, me, mo, rsv;
+};
+__device__ __forceinline__ void count_add(Counts& c, uint32_t w) {
+    c.pe += w & 0x11111111u;
+    c.me += (w >> 1) & 0x11111111u;
+    c.po += (w >> 2) & 0x11111111u;
+    c.mo += (w >> 3) & 0x11111111u;
+    c.rsv |= w & (w >> 1) & 0x55555555u;
+}
+// signed count for code position j (0..15)
+__device__ __forceinline__ int count_at(const Counts& c, int j) {
+    const int sh = 4 * (j >> 1);
+    const uint32_t p = (j & 1) ? c.po : c.pe;
+    const uint32_t m = (j & 1) ? c.mo : c.me;
+    return static_cast<int>((p >> sh) & 15u) - static_cast<int>((m >> sh) & 15u);
+}
+__device__ __forceinline__ double decode1(uint32_t code, double alpha) {
+    return code == 1u ? alpha : (code == 2u ? -alpha : 0.0);
+}
+
+// ================================================================ K2: apply_quant
+// Fused: decode N gathered payloads, ascending-rank fp64 sum / N (engine.py:249-255),
+// W' = W - eta_g*mean (engine.py:511) on fp32 W, loc = W' - eta_l*g_next (Eq. 11,
+// engine.py:385-392), optional sum(mean^2) (engine.py:521).
+struct ApplyQArgs {
+    float* W;
+    const uint32_t* gathered;
+    int64_t stride;  // words between ranks
+    const float* gnext;
+    float* loc;
+    double alpha, inv_n_or_zero, eta_g_d, eta_l_d;  // inv_n_or_zero: 1/N if N is pow2 else 0
+    float eta_l;
+    int nranks;
+    int exact;  // exact-alpha table mode
+    uint64_t* err;
+    uint64_t skip_below;
+    double* gnorm;
+};
+
+__device__ __forceinline__ double apply_mean_general(const uint32_t* codes, int nr, double alpha,
+                                                     double inv_n, bool& rsv) {
+    double tot = 0.0;
+    for (int r = 0; r < nr; ++r) {
+        const uint32_t c = codes[r];
+        rsv |= c == 3u;
+        const double d = decode1(c, alpha);
+        tot = r == 0 ? d : __dadd_rn(tot, d);
+    }
+    return inv_n != 0.0 ? __dmul_rn(tot, inv_n) : __ddiv_rn(tot, static_cast<double>(nr));
+}
+
+template <int NR>  // NR > 0: compile-time rank count; NR == 0: runtime (generic)
+__global__ void __launch_bounds__(256) k_apply_quant(ApplyQArgs a, KeyTab kt, DecodeTab tab) {
+    if (a.err != nullptr && *reinterpret_cast<volatile uint64_t*>(a.err) < a.skip_below) return;
+    __shared__ double s_mean[2 * MAX_RANKS + 1];
+    __shared__ float s_upd[2 * MAX_RANKS + 1];
+    const int nr = NR > 0 ? NR : a.nranks;
+    if (threadIdx.x < 2 * nr + 1) {
+        s_mean[threadIdx.x] = tab.mean[threadIdx.x];
+        s_upd[threadIdx.x] = tab.upd[threadIdx.x];
+    }
+    __syncthreads();
+    int64_t tb, te;
+    warp_range(kt.ntiles, tb, te);
+    const int lane = threadIdx.x & 31;
+    double gsq = 0.0;
+    uint64_t bad_idx = NO_ERR;
+    const bool do_loc = a.loc != nullptr;
+    if (tb < te) {
+        TileCursor kc;
+        kc.seek(kt, tb);
+        for (int64_t ti = tb; ti < te; ++ti) {
+            kc.advance_to(kt, ti);
+            const int64_t j = ti - kc.t0;
+            const int64_t e0 = kc.e0 + j * TILE_ELEMS;
+            const int64_t w0 = kc.w0 + j * TILE_WORDS;
+            const int64_t ne64 = kc.e1 - e0;
+            const int ne = ne64 < TILE_ELEMS ? static_cast<int>(ne64) : TILE_ELEMS;
+            const int64_t nw64 = kc.w1 - w0;
+            const int nw = nw64 < TILE_WORDS ? static_cast<int>(nw64) : TILE_WORDS;
+            const bool fast = NR > 0 && a.exact && ne == TILE_ELEMS && aligned_to(a.W + e0, 16) &&
+                              (!do_loc || (aligned_to(a.gnext + e0, 16) && aligned_to(a.loc + e0, 16)));
+            if (fast) {
+                constexpr int R = NR > 0 ? NR : 1;
+                uint32_t wv[R];
+#pragma unroll
+                for (int r = 0; r < R; ++r) wv[r] = ld_word(a.gathered + r * a.stride + w0 + lane);
+                float4 wt[CHUNKS], gt[CHUNKS];
+#pragma unroll
+                for (int c = 0; c < CHUNKS; ++c) {
+                    const int64_t e = e0 + 128 * c + 4 * lane;
+                    wt[c] = ld_stream(a.W + e);
+                    if (do_loc) gt[c] = ld_stream(a.gnext + e);
+                }
+#pragma unroll
+                for (int c = 0; c < CHUNKS; ++c) {
+                    const int64_t e = e0 + 128 * c + 4 * lane;
+                    Counts cnt{0u, 0u, 0u, 0u, 0u};
+#pragma unroll
+                    for (int r = 0; r < R; ++r) count_add(cnt, __shfl_sync(FULL, wv[r], 8 * c + (lane >> 2)));
+                    const int jb = 4 * (lane & 3);  // first code position of this lane in the word
+                    float w4[4] = {wt[c].x, wt[c].y, wt[c].z, wt[c].w};
+                    float g4[4];
+                    if (do_loc) { g4[0] = gt[c].x; g4[1] = gt[c].y; g4[2] = gt[c].z; g4[3] = gt[c].w; }
+                    float l4[4];
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const int ci = count_at(cnt, jb + q) + nr;
+                        w4[q] = __fsub_rn(w4[q], s_upd[ci]);
+                        if (do_loc) l4[q] = __fmaf_rn(-a.eta_l, g4[q], w4[q]);
+                        if (a.gnorm != nullptr) {
+                            const double mv = s_mean[ci];
+                            gsq = __fma_rn(mv, mv, gsq);
+                        }
+                    }
+                    if (((cnt.rsv >> (2 * jb)) & 0xffu) != 0u) {
+                        const int q = __ffs((cnt.rsv >> (2 * jb)) & 0x55u) / 2;
+                        const uint64_t idx = static_cast<uint64_t>(e + q);
+                        bad_idx = idx < bad_idx ? idx : bad_idx;
+                    }
+                    st_stream(a.W + e, w4[0], w4[1], w4[2], w4[3]);
+                    if (do_loc) st_stream(a.loc + e, l4[0], l4[1], l4[2], l4[3]);
+                }
+            } else {
+                // generic path: lane l owns element 32s + l; word (2s + l/16), code l%16
+                uint32_t wv[MAX_RANKS];
+                const bool wl = lane < nw;
+                for (int r = 0; r < nr; ++r) wv[r] = wl ? a.gathered[r * a.stride + w0 + lane] : 0u;
+#pragma unroll 2
+                for (int s = 0; s < TILE_ELEMS / 32; ++s) {
+                    const int el = 32 * s + lane;
+                    uint32_t codes[MAX_RANKS];
+                    for (int r = 0; r < nr; ++r)
+                        codes[r] = (__shfl_sync(FULL, wv[r], 2 * s + (lane >> 4)) >> (2 * (lane & 15))) & 3u;
+                    if (el < ne) {
+                        const int64_t e = e0 + el;
+                        bool rsv = false;
+                        double mean;
+                        float upd;
+                        if (a.exact) {
+                            int cn = 0;
+                            for (int r = 0; r < nr; ++r) {
+                                rsv |= codes[r] == 3u;
+                                cn += (codes[r] == 1u) - (codes[r] == 2u);
+                            }
+                            mean = s_mean[cn + nr];
+                            upd = s_upd[cn + nr];
+                        } else {
+                            mean = apply_mean_general(codes, nr, a.alpha, a.inv_n_or_zero, rsv);
+                            upd = __double2float_rn(__dmul_rn(a.eta_g_d, mean));
+                        }
+                        const float wn = __fsub_rn(a.W[e], upd);
+                        a.W[e] = wn;
+                        if (do_loc) a.loc[e] = __fmaf_rn(-a.eta_l, a.gnext[e], wn);
+                        if (a.gnorm != nullptr) gsq = __fma_rn(mean, mean, gsq);
+                        if (rsv) bad_idx = static_cast<uint64_t>(e) < bad_idx ? static_cast<uint64_t>(e) : bad_idx;
+                    }
+                }
+            }
+        }
+    }
+    if (a.gnorm != nullptr) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) gsq += __shfl_xor_sync(FULL, gsq, o);
+        if (lane == 0 && gsq != 0.0) atomicAdd(a.gnorm, gsq);
+    }
+    if (a.err != nullptr) {
+        bad_idx = warp_min_u64(bad_idx);
+        if (lane == 0 && bad_idx != NO_ERR)
+            atomicMin(reinterpret_cast<unsigned long long*>(a.err + 1), static_cast<unsigned long long>(bad_idx));
+    }
+}
+
+// ================================================================ dequantize / aggregate
+// codec.dequantize (n = 1) and server_aggregate's quantized branch: fp64 out.
+__global__ void __launch_bounds__(256) k_dequant_sum(const uint32_t* __restrict__ words, int nr,
+                                                     int64_t stride, KeyTab kt, double alpha,
+                                                     double* __restrict__ out, uint64_t* err) {
+    int64_t tb, te;
+    warp_range(kt.ntiles, tb, te);
+    if (tb >= te) return;
+    const int lane = threadIdx.x & 31;
+    const double inv_n = (nr & (nr - 1)) == 0 ? 1.0 / nr : 0.0;
+    TileCursor kc;
+    kc.seek(kt, tb);
+    uint64_t bad_idx = NO_ERR;
+    for (int64_t ti = tb; ti < te; ++ti) {
+        kc.advance_to(kt, ti);
+        const int64_t j = ti - kc.t0;
+        const int64_t e0 = kc.e0 + j * TILE_ELEMS;
+        const int64_t w0 = kc.w0 + j * TILE_WORDS;
+        const int64_t ne64 = kc.e1 - e0;
+        const int ne = ne64 < TILE_ELEMS ? static_cast<int>(ne64) : TILE_ELEMS;
+        const int64_t nw64 = kc.w1 - w0;
+        const int nw = nw64 < TILE_WORDS ? static_cast<int>(nw64) : TILE_WORDS;
+        for (int s = 0; s < TILE_ELEMS / 32; ++s) {
+            const int el = 32 * s + lane;
+            const int wi = 2 * s + (lane >> 4);
+            if (el < ne && wi < nw) {
+                double tot = 0.0;
+                bool rsv = false;
+                for (int r = 0; r < nr; ++r) {
+                    const uint32_t c = (words[r * stride + w0 + wi] >> (2 * (lane & 15))) & 3u;
+                    rsv |= c == 3u;
+                    const double d = decode1(c, alpha);
+                    tot = r == 0 ? d : __dadd_rn(tot, d);
+                }
+                out[e0 + el] = inv_n != 0.0 ? __dmul_rn(tot, inv_n) : __ddiv_rn(tot, static_cast<double>(nr));
+                if (rsv) bad_idx = static_cast<uint64_t>(e0 + el) < bad_idx ? static_cast<uint64_t>(e0 + el) : bad_idx;
+            }
+        }
+    }
+    if (err != nullptr) {
+        bad_idx = warp_min_u64(bad_idx);
+        if (lane == 0 && bad_idx != NO_ERR)
+            atomicMin(reinterpret_cast<unsigned long long*>(err), static_cast<unsigned long long>(bad_idx));
+    }
+}
+
+template <typename G>
+__global__ void k_aggregate_full(const G* __restrict__ grads, int nc, int64_t stride, int64_t n,
+                                 double* __restrict__ out) {
+    const double inv_n = (nc & (nc - 1)) == 0 ? 1.0 / nc : 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        double tot = static_cast<double>(grads[i]);
+        for (int c = 1; c < nc; ++c) tot = __dadd_rn(tot, static_cast<double>(grads[c * stride + i]));
+        out[i] = inv_n != 0.0 ? __dmul_rn(tot, inv_n) : __ddiv_rn(tot, static_cast<double>(nc));
+    }
+}
+
+// ================================================================ pack / unpack
+__global__ void k_pack(const uint8_t* __restrict__ sym, int64_t n, uint32_t* __restrict__ words,
+                       uint64_t* err) {
+    const int64_t nw = (n + 15) / 16;
+    uint64_t bad_idx = NO_ERR;
+    for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < nw; w += (int64_t)gridDim.x * blockDim.x) {
+        uint32_t v = 0;
+        for (int j = 0; j < 16; ++j) {
+            const int64_t i = 16 * w + j;
+            if (i < n) {
+                const uint32_t s = sym[i];
+                if (s > 2u && static_cast<uint64_t>(i) < bad_idx) bad_idx = static_cast<uint64_t>(i);
+                v |= (s & 3u) << (2 * j);
+            }
+        }
+        words[w] = v;
+    }
+    if (err != nullptr && bad_idx != NO_ERR)
+        atomicMin(reinterpret_cast<unsigned long long*>(err), static_cast<unsigned long long>(bad_idx));
+}
+
+__global__ void k_unpack(const uint32_t* __restrict__ words, int64_t length, uint8_t* __restrict__ sym) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < length; i += (int64_t)gridDim.x * blockDim.x)
+        sym[i] = static_cast<uint8_t>((words[i >> 4] >> (2 * (i & 15))) & 3u);
+}
+
+// ================================================================ K3: apply_full + elementwise
+// Correction round: W' = W - (eta_g/N)*gsum ; loc = W' - eta_l*g_next.
+struct ApplyFArgs {
+    float* W;
+    const float* gsum;
+    const float* gnext;
+    float* loc;
+    float scale;   // (float)(eta_g / N)
+    float eta_l;
+    double inv_n;  // for the grad-norm metric
+    int64_t n;
+    const uint64_t* err;
+    uint64_t skip_below;
+    double* gnorm;
+};
+
+__global__ void __launch_bounds__(256) k_apply_full(ApplyFArgs a) {
+    if (a.err != nullptr && *reinterpret_cast<volatile const uint64_t*>(a.err) < a.skip_below) return;
+    const bool do_loc = a.loc != nullptr;
+    const bool vec = aligned_to(a.W, 16) && aligned_to(a.gsum, 16) &&
+                     (!do_loc || (aligned_to(a.gnext, 16) && aligned_to(a.loc, 16)));
+    const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t nth = (int64_t)gridDim.x * blockDim.x;
+    double gsq = 0.0;
+    int64_t done = 0;
+    if (vec) {
+        const int64_t nv = a.n / 4;
+        constexpr int U = 2;
+        int64_t i = tid;
+        for (; i + (U - 1) * nth < nv; i += U * nth) {
+            float4 w[U], s[U], g[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                w[u] = ld_stream(a.W + 4 * (i + u * nth));
+                s[u] = ld_stream(a.gsum + 4 * (i + u * nth));
+                if (do_loc) g[u] = ld_stream(a.gnext + 4 * (i + u * nth));
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                float4 o;
+                o.x = __fmaf_rn(-a.scale, s[u].x, w[u].x);
+                o.y = __fmaf_rn(-a.scale, s[u].y, w[u].y);
+                o.z = __fmaf_rn(-a.scale, s[u].z, w[u].z);
+                o.w = __fmaf_rn(-a.scale, s[u].w, w[u].w);
+                st_stream(a.W + 4 * (i + u * nth), o.x, o.y, o.z, o.w);
+                if (do_loc)
+                    st_stream(a.loc + 4 * (i + u * nth), __fmaf_rn(-a.eta_l, g[u].x, o.x),
+                              __fmaf_rn(-a.eta_l, g[u].y, o.y), __fmaf_rn(-a.eta_l, g[u].z, o.z),
+                              __fmaf_rn(-a.eta_l, g[u].w, o.w));
+                if (a.gnorm != nullptr) {
+                    const double m0 = s[u].x * a.inv_n, m1 = s[u].y * a.inv_n, m2 = s[u].z * a.inv_n,
+                                 m3 = s[u].w * a.inv_n;
+                    gsq += m0 * m0 + m1 * m1 + m2 * m2 + m3 * m3;
+                }
+            }
+        }
+        for (; i < nv; i += nth) {
+            float4 w = ld_stream(a.W + 4 * i), s = ld_stream(a.gsum + 4 * i);
+            float4 o;
+            o.x = __fmaf_rn(-a.scale, s.x, w.x);
+            o.y = __fmaf_rn(-a.scale, s.y, w.y);
+            o.z = __fmaf_rn(-a.scale, s.z, w.z);
+            o.w = __fmaf_rn(-a.scale, s.w, w.w);
+            st_stream(a.W + 4 * i, o.x, o.y, o.z, o.w);
+            if (do_loc) {
+                float4 g = ld_stream(a.gnext + 4 * i);
+                st_stream(a.loc + 4 * i, __fmaf_rn(-a.eta_l, g.x, o.x), __fmaf_rn(-a.eta_l, g.y, o.y),
+                          __fmaf_rn(-a.eta_l, g.z, o.z), __fmaf_rn(-a.eta_l, g.w, o.w));
+            }
+            if (a.gnorm != nullptr) {
+                const double m0 = s.x * a.inv_n, m1 = s.y * a.inv_n, m2 = s.z * a.inv_n, m3 = s.w * a.inv_n;
+                gsq += m0 * m0 + m1 * m1 + m2 * m2 + m3 * m3;
+            }
+        }
+        done = nv * 4;
+    }
+    for (int64_t i = done + tid; i < a.n; i += nth) {
+        const float s = a.gsum[i];
+        const float wn = __fmaf_rn(-a.scale, s, a.W[i]);
+        a.W[i] = wn;
+        if (do_loc) a.loc[i] = __fmaf_rn(-a.eta_l, a.gnext[i], wn);
+        if (a.gnorm != nullptr) { const double m = s * a.inv_n; gsq += m * m; }
+    }
+    if (a.gnorm != nullptr) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) gsq += __shfl_xor_sync(FULL, gsq, o);
+        if ((threadIdx.x & 31) == 0 && gsq != 0.0) atomicAdd(a.gnorm, gsq);
+    }
+}
+
+// engine.global_update / local_update with fp64 math (exact reference arithmetic
+// for fp64 operands; one rounding to the output type otherwise).
+template <typename T> __device__ __forceinline__ double to_d(T v) { return static_cast<double>(v); }
+template <typename T> __device__ __forceinline__ T from_d(double v);
+template <> __device__ __forceinline__ float from_d<float>(double v) { return __double2float_rn(v); }
+template <> __device__ __forceinline__ double from_d<double>(double v) { return v; }
+
+template <typename TW, typename TM>
+__global__ void k_global_update(TW* __restrict__ w, const TM* __restrict__ mean, int64_t n, double eta) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        w[i] = from_d<TW>(__dsub_rn(to_d(w[i]), __dmul_rn(eta, to_d(mean[i]))));
+}
+
+template <typename TB, typename TG, typename TO>
+__global__ void k_local_update(const TB* __restrict__ base, const TG* __restrict__ g, TO* __restrict__ out,
+                               int64_t n, double eta_l) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = from_d<TO>(__dsub_rn(to_d(base[i]), __dmul_rn(eta_l, to_d(g[i]))));
+}
+
+}  // namespace cdsgd

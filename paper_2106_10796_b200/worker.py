@@ -1,0 +1,219 @@
+"""Per-GPU CD-SGD worker: the fused quantize -> exchange -> apply step driver.
+
+One process per GPU; each rank is one CD-SGD worker (Algorithm 1) AND a replica of
+the parameter server: it keeps the global weights W (fp32, bitwise identical on
+every rank), its own fp64 residual, local weights and packed-code buffers, and
+drives the native ``cdsgd_engine`` of libcdsgd_b200.so (include/cdsgd_b200.h).
+
+Semantics follow Worker/ServerNode/_run_lockstep (engine.py:288-663) with the
+gradient supplied by the caller instead of ``loss_and_grad`` (engine.py:363):
+
+    w = CDSGDWorker(layout, hp, w0, rank=r, comm=comm)
+    for t in range(T):
+        x = w.compute_weights()        # engine.py:335-343 (W during warm-up, else loc)
+        g = my_gradient(x)             # fp32 CUDA tensor [layout.total]
+        w.step(g)                      # K1 + exchange(t) || K2/K3(t-1) + local update
+    w.flush()                          # W == W_T (ServerNode.weights after T rounds)
+
+Round t's exchange runs on the engine's stream while the caller computes the
+gradient of round t+1 at loc_{t+1} = W_t - eta_l * g_t (the paper's overlap).
+Numeric errors are detected on the device and raised by ``check()`` (called by
+``flush()`` and every ``check_every`` rounds) as CodecNumericError with the key,
+key-local index and round; the residual is rolled back to the state before it.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+import torch
+
+from . import _lib
+from .codec import CodecNumericError, CorruptPayloadError, _locate
+from .engine import ConfigError, HyperParams, SchedulingError
+from .layout import Layout
+
+
+class CDSGDWorker:
+    def __init__(
+        self,
+        layout: Layout,
+        hp: HyperParams,
+        init_weights,
+        *,
+        rank: int = 0,
+        comm=None,
+        force_compress: bool = False,
+        bypass_local: bool = False,
+        gnorm_ring: int = 64,
+        check_every: int = 0,
+        device=None,
+    ):
+        if not torch.cuda.is_available():
+            raise _lib.LibraryError("CDSGDWorker needs a CUDA device (no CPU fallback)")
+        hp.validate()
+        self.hp = hp
+        self.layout = layout
+        self.rank = rank
+        self.world = hp.workers
+        if self.world > 1 and comm is None:
+            raise ConfigError("workers > 1 needs an NCCL Comm (paper_2106_10796_b200.comm.Comm)")
+        if comm is not None and (comm.world != self.world or comm.rank != rank):
+            raise ConfigError("comm size/rank do not match hp.workers/rank")
+        self.comm = comm
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        dev = self.device
+        n, nw = layout.total, layout.n_words
+        w0 = init_weights if isinstance(init_weights, torch.Tensor) else torch.from_numpy(np.asarray(init_weights))
+        if w0.numel() != n:
+            raise ConfigError(f"initial weights have {w0.numel()} elements, layout needs {n}")
+        with torch.cuda.device(dev):
+            self.W = w0.reshape(-1).to(device=dev, dtype=torch.float32).clone()
+            self.loc = self.W.clone()
+            self.residuals = [torch.zeros(n, dtype=torch.float64, device=dev), torch.empty(n, dtype=torch.float64, device=dev)]
+            self.gathered = [torch.zeros(self.world * nw, dtype=torch.int32, device=dev).view(torch.uint32) for _ in range(2)]
+            self.gsum = [torch.empty(n, dtype=torch.float32, device=dev) for _ in range(2)] if self.world > 1 else [None, None]
+            self.err = torch.full((2,), -1, dtype=torch.int64, device=dev)
+            self.gnorm_ring = max(int(gnorm_ring), 0)
+            self.gnorm = torch.zeros(max(self.gnorm_ring, 1), dtype=torch.float64, device=dev)
+            d = _lib.EngineDesc()
+            d.algo = _lib.ALGO[hp.algo]
+            d.nranks = self.world
+            d.rank = rank
+            d.k = hp.k
+            d.warmup_n = hp.warmup_n
+            d.force_compress = int(force_compress)
+            d.bypass_local = int(bypass_local)
+            d.gnorm_ring = self.gnorm_ring
+            d.alpha = float(hp.alpha)
+            d.eta_global = float(hp.eta_global)
+            d.eta_local = float(hp.local_lr)
+            d.weights = self.W.data_ptr()
+            d.loc = self.loc.data_ptr()
+            d.residual[0] = self.residuals[0].data_ptr()
+            d.residual[1] = self.residuals[1].data_ptr()
+            d.gathered[0] = self.gathered[0].data_ptr()
+            d.gathered[1] = self.gathered[1].data_ptr()
+            d.gsum[0] = self.gsum[0].data_ptr() if self.gsum[0] is not None else None
+            d.gsum[1] = self.gsum[1].data_ptr() if self.gsum[1] is not None else None
+            d.err = self.err.data_ptr()
+            d.gnorm_sq = self.gnorm.data_ptr() if self.gnorm_ring else None
+            self._desc = d
+            out = C.c_void_p()
+            _lib.check(
+                _lib.lib().cdsgd_engine_create(C.byref(d), layout.handle(dev.index).ptr,
+                                               comm.ptr if comm is not None else None, C.byref(out)),
+                "cdsgd_engine_create",
+            )
+            self._eng = out
+        self._keep: list[torch.Tensor] = []  # gradients still read by in-flight rounds
+        self.check_every = int(check_every)
+        self._since_check = 0
+        self._lib = _lib.lib()
+
+    # ------------------------------------------------------------------ state
+    def state(self) -> _lib.EngineState:
+        st = _lib.EngineState()
+        _lib.check(self._lib.cdsgd_engine_get_state(self._eng, C.byref(st)), "engine_get_state")
+        return st
+
+    @property
+    def t(self) -> int:
+        return int(self.state().t)
+
+    @property
+    def residual(self) -> torch.Tensor:
+        """The live fp64 residual (concatenated over keys)."""
+        return self.residuals[self.state().residual_index]
+
+    @property
+    def weights(self) -> torch.Tensor:
+        """Global weights replica (W_t once every started round is applied, see flush())."""
+        return self.W
+
+    def compute_weights(self) -> torch.Tensor:
+        """Weights the next gradient must be computed at (engine.py:335-343)."""
+        return self.loc if self.state().compute_is_loc else self.W
+
+    def round_compressed(self, t: int) -> bool:
+        r = self._lib.cdsgd_engine_round_compressed(self._eng, int(t))
+        if r < 0:
+            raise ConfigError(_lib.last_error())
+        return bool(r)
+
+    def grad_norm(self, t: int) -> float:
+        """||round-t mean gradient||_2 (engine.py:521); valid for the last gnorm_ring rounds."""
+        if not self.gnorm_ring:
+            raise ConfigError("grad-norm metric disabled (gnorm_ring=0)")
+        return float(self.gnorm[t % self.gnorm_ring].sqrt().item())
+
+    # ------------------------------------------------------------------ driving
+    def step(self, grad: torch.Tensor) -> None:
+        if grad.dtype != torch.float32 or not grad.is_cuda or not grad.is_contiguous() or grad.numel() != self.layout.total:
+            raise ConfigError("gradient must be a contiguous fp32 CUDA tensor of layout.total elements")
+        rc = self._lib.cdsgd_engine_step(self._eng, grad.data_ptr(), torch.cuda.current_stream(self.device).cuda_stream)
+        if rc != _lib.OK:
+            msg = _lib.last_error()
+            if rc == _lib.ERR_STATE:
+                raise SchedulingError(msg)
+            if rc == _lib.ERR_ARG:
+                raise ConfigError(msg)
+            raise _lib.LibraryError(msg, rc)
+        self._keep.append(grad)
+        if len(self._keep) > 2:
+            del self._keep[0]
+        if self.check_every:
+            self._since_check += 1
+            if self._since_check >= self.check_every:
+                self.check()
+
+    def flush(self) -> None:
+        """Apply the last exchanged round: afterwards W == W_t."""
+        _lib.check(self._lib.cdsgd_engine_flush(self._eng, torch.cuda.current_stream(self.device).cuda_stream), "flush")
+        self.check()
+
+    def check(self) -> None:
+        """Synchronise and raise the first device-side error (CodecNumericError / CorruptPayloadError)."""
+        rnd, idx = C.c_int64(-1), C.c_int64(-1)
+        rc = self._lib.cdsgd_engine_check(self._eng, torch.cuda.current_stream(self.device).cuda_stream,
+                                          C.byref(rnd), C.byref(idx))
+        self._since_check = 0
+        if rc == _lib.OK:
+            return
+        if rc == _lib.ERR_NUMERIC:
+            key, local = _locate(self.layout, int(idx.value))
+            raise CodecNumericError(
+                f"non-finite accumulated gradient at element {local} (key {key}, round {rnd.value})",
+                local, key=key, round=int(rnd.value),
+            )
+        if rc == _lib.ERR_CORRUPT:
+            raise CorruptPayloadError(_lib.last_error())
+        raise _lib.LibraryError(_lib.last_error(), rc)
+
+    def join(self, stream=None) -> None:
+        """Make `stream` (default: current) wait for every exchange issued so far."""
+        st = (stream or torch.cuda.current_stream(self.device)).cuda_stream
+        _lib.check(self._lib.cdsgd_engine_join(self._eng, st), "join")
+
+    def profile_begin(self) -> None:
+        """Start recording CUDA events around every kernel / NCCL call of the step."""
+        _lib.check(self._lib.cdsgd_engine_profile_begin(self._eng), "profile_begin")
+
+    def profile_end(self) -> dict:
+        """Per-kernel-class total ms and launch counts since profile_begin()."""
+        out = (C.c_double * 10)()
+        _lib.check(self._lib.cdsgd_engine_profile_end(self._eng, out), "profile_end")
+        names = ("quantize", "apply_quant", "apply_full", "local_update", "exchange")
+        return {nm: {"ms": out[2 * i], "n": int(out[2 * i + 1])} for i, nm in enumerate(names)}
+
+    def close(self) -> None:
+        if getattr(self, "_eng", None):
+            _lib.lib().cdsgd_engine_destroy(self._eng)
+            self._eng = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
