@@ -8,11 +8,13 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
 #include "cdsgd_b200.h"
 #include "kernels.cuh"
+#include "kernels_tma.cuh"
 
 using namespace cdsgd;
 
@@ -86,6 +88,106 @@ int flat_grid(K kernel, int64_t work) {
     return static_cast<int>(want < cap ? (want > 0 ? want : 1) : cap);
 }
 inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// TMA-staged kernels: one 256-thread CTA per SM, dynamic smem ring.
+bool use_ldg() {
+    static const bool v = [] {
+        const char* e = getenv("CDSGD_LDG");
+        return e != nullptr && e[0] == '1';
+    }();
+    return v;
+}
+template <typename K>
+bool prepare_tma(K kernel, int smem_bytes) {
+    int d = 0;
+    cudaGetDevice(&d);
+    // cudaFuncSetAttribute is cheap but not free; remember per (kernel, device)
+    struct Key { const void* k; int d; };
+    static thread_local Key seen[64];
+    static thread_local int nseen = 0;
+    for (int i = 0; i < nseen; ++i)
+        if (seen[i].k == reinterpret_cast<const void*>(kernel) && seen[i].d == d) return true;
+    if (cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes) != cudaSuccess)
+        return false;
+    if (nseen < 64) seen[nseen++] = Key{reinterpret_cast<const void*>(kernel), d};
+    return true;
+}
+inline int tma_grid(int64_t ntiles, int warps) {
+    const int64_t want = (ntiles + warps - 1) / warps;
+    const int64_t cap = dev_info().sms;
+    return static_cast<int>(want < cap ? (want > 0 ? want : 1) : cap);
+}
+// Tuning knobs for development sweeps: CDSGD_TMA_CFG (K1) / CDSGD_TMA_CFG2 (K2, K3) = <warps>x<stages>.
+int read_cfg(const char* name, int dflt) {
+    const char* e = getenv(name);
+    int w = 0, st = 0;
+    if (e == nullptr || sscanf(e, "%dx%d", &w, &st) != 2) return dflt;
+    return w * 10 + st;
+}
+int tma_cfg() {
+    static const int v = read_cfg("CDSGD_TMA_CFG", 162);
+    return v;
+}
+int tma_cfg2() {
+    static const int v = read_cfg("CDSGD_TMA_CFG2", 84);
+    return v;
+}
+template <int NR, int WP, int ST>
+int launch_aq_tma(const ApplyQArgs& a, const KeyTab& kt, const DecodeTab& tab, cudaStream_t st) {
+    using SM = ApplyQSmem<NR, WP, ST>;
+    static_assert(SM::BYTES <= 227 * 1024, "smem");
+    if (!prepare_tma(k_apply_quant_tma<NR, WP, ST>, SM::BYTES)) return fail(CDSGD_ERR_CUDA, "smem attribute");
+    k_apply_quant_tma<NR, WP, ST><<<tma_grid(kt.ntiles, WP), WP * 32, SM::BYTES, st>>>(a, kt, tab);
+    return CDSGD_OK;
+}
+template <int NR>
+int launch_aq_tma_cfg(const ApplyQArgs& a, const KeyTab& kt, const DecodeTab& tab, cudaStream_t st) {
+    switch (tma_cfg2()) {
+        case 162: return launch_aq_tma<NR, 16, 2>(a, kt, tab, st);
+        case 83: return launch_aq_tma<NR, 8, 3>(a, kt, tab, st);
+        default: return launch_aq_tma<NR, 8, 4>(a, kt, tab, st);
+    }
+}
+template <int WP, int ST>
+int launch_af_tma(const ApplyFArgs& a, cudaStream_t st) {
+    using SM = ApplyFSmem<WP, ST>;
+    static_assert(SM::BYTES <= 227 * 1024, "smem");
+    if (!prepare_tma(k_apply_full_tma<WP, ST>, SM::BYTES)) return fail(CDSGD_ERR_CUDA, "smem attribute");
+    k_apply_full_tma<WP, ST><<<tma_grid((a.n + TILE_ELEMS - 1) / TILE_ELEMS, WP), WP * 32, SM::BYTES, st>>>(a);
+    return CDSGD_OK;
+}
+int launch_af_tma_cfg(const ApplyFArgs& a, cudaStream_t st) {
+    switch (tma_cfg2()) {
+        case 162: return launch_af_tma<16, 2>(a, st);
+        case 83: return launch_af_tma<8, 3>(a, st);
+        default: return launch_af_tma<8, 4>(a, st);
+    }
+}
+template <typename G, int WARPS, int ST>
+int launch_quant_tma(const G* g, const double* r_in, double* r_out, uint32_t* words, KeyTab kt, double alpha,
+                     uint64_t* err, uint64_t tag, cudaStream_t st) {
+    using SM = QuantSmem<G, WARPS, ST>;
+    static_assert(SM::BYTES <= 227 * 1024, "smem");
+    if (!prepare_tma(k_quantize_tma<G, WARPS, ST>, SM::BYTES)) return fail(CDSGD_ERR_CUDA, "smem attribute");
+    k_quantize_tma<G, WARPS, ST><<<tma_grid(kt.ntiles, WARPS), WARPS * 32, SM::BYTES, st>>>(g, r_in, r_out, words, kt,
+                                                                                          alpha, err, tag);
+    return CDSGD_OK;
+}
+template <typename G>
+int launch_quant_tma_cfg(const G* g, const double* r_in, double* r_out, uint32_t* words, KeyTab kt, double alpha,
+                         uint64_t* err, uint64_t tag, cudaStream_t st) {
+    if constexpr (sizeof(G) == 8) {
+        return launch_quant_tma<G, 8, 3>(g, r_in, r_out, words, kt, alpha, err, tag, st);
+    } else {
+    switch (tma_cfg()) {
+        case 43: return launch_quant_tma<G, 4, 3>(g, r_in, r_out, words, kt, alpha, err, tag, st);
+        case 46: return launch_quant_tma<G, 4, 6>(g, r_in, r_out, words, kt, alpha, err, tag, st);
+        case 83: return launch_quant_tma<G, 8, 3>(g, r_in, r_out, words, kt, alpha, err, tag, st);
+        case 84: return launch_quant_tma<G, 8, 4>(g, r_in, r_out, words, kt, alpha, err, tag, st);
+        default: return launch_quant_tma<G, 16, 2>(g, r_in, r_out, words, kt, alpha, err, tag, st);
+    }
+    }
+}
 }  // namespace
 
 // ------------------------------------------------------------------ layout
@@ -173,6 +275,18 @@ extern "C" int cdsgd_quantize(const cdsgd_layout* L, const void* grad, int32_t g
     if (L->n == 0) return CDSGD_OK;
     if (!grad || !r_in || !r_out || !words) return fail(CDSGD_ERR_ARG, "NULL buffer");
     const KeyTab kt = L->tab();
+    if (!use_ldg()) {
+        int rc;
+        if (gdt == CDSGD_F32)
+            rc = launch_quant_tma_cfg(static_cast<const float*>(grad), r_in, r_out, words, kt, alpha, err, tag, S(stream));
+        else if (gdt == CDSGD_F64)
+            rc = launch_quant_tma_cfg(static_cast<const double*>(grad), r_in, r_out, words, kt, alpha, err, tag, S(stream));
+        else
+            return fail(CDSGD_ERR_ARG, "grad dtype must be CDSGD_F32 or CDSGD_F64");
+        if (rc != CDSGD_OK) return rc;
+        LAUNCH_CHECK();
+        return CDSGD_OK;
+    }
     if (gdt == CDSGD_F32) {
         const int grid = tile_grid(k_quantize<float>, kt.ntiles);
         k_quantize<float><<<grid, THREADS, 0, S(stream)>>>(static_cast<const float*>(grad), r_in, r_out, words,
@@ -332,6 +446,20 @@ int launch_apply_quant(const cdsgd_layout* L, float* W, const uint32_t* gathered
     }
     a.exact = exact;
     const KeyTab kt = L->tab();
+    static const bool k2_tma = [] {
+        const char* e = getenv("CDSGD_K2_TMA");
+        return e != nullptr && e[0] == '1';
+    }();
+    if (k2_tma && exact && nr <= 8) {
+        int rc = CDSGD_OK;
+#define AQT(R)                                               \
+    case R: rc = launch_aq_tma_cfg<R>(a, kt, tab, st); break;
+        switch (nr) { AQT(1) AQT(2) AQT(3) AQT(4) AQT(5) AQT(6) AQT(7) AQT(8) }
+        if (rc != CDSGD_OK) return rc;
+#undef AQT
+        LAUNCH_CHECK();
+        return CDSGD_OK;
+    }
 #define AQ(R)                                                                                   \
     case R:                                                                                     \
         k_apply_quant<R><<<tile_grid(k_apply_quant<R>, kt.ntiles), THREADS, 0, st>>>(a, kt, tab); \
@@ -364,6 +492,12 @@ int launch_apply_full(float* W, const float* gsum, int nr, int64_t n, double eta
     a.err = err;
     a.skip_below = skip_below;
     a.gnorm = gnorm;
+    if (!use_ldg()) {
+        const int rc = launch_af_tma_cfg(a, st);
+        if (rc != CDSGD_OK) return rc;
+        LAUNCH_CHECK();
+        return CDSGD_OK;
+    }
     k_apply_full<<<flat_grid(k_apply_full, (n + 7) / 8), THREADS, 0, st>>>(a);
     LAUNCH_CHECK();
     return CDSGD_OK;

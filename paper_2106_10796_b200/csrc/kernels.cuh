@@ -162,6 +162,27 @@ __device__ __forceinline__ uint32_t quant1(double r, G g, double alpha, double& 
     return p ? 1u : (m ? 2u : 0u);
 }
 
+// Lean form of quant1 for the staged fast path (same bits, fewer instructions):
+//   nz = |acc| >= alpha  (== plus || minus for non-NaN acc)
+//   r' = nz ? acc + s : acc,  s = -copysign(alpha, acc)   (x + (-y) == x - y exactly,
+//        so this is acc - alpha on plus, acc - (-alpha) on minus; ties give +0.0 as
+//        in the reference; acc = -0.0 passes through unchanged)
+//   code = nz ? 1 + signbit(acc) : 0
+// Non-finite accumulators only raise `bad` (the caller rescans for the index).
+template <typename G>
+__device__ __forceinline__ uint32_t quant1_lean(double r, G g, double alpha, uint32_t alpha_hi, uint32_t alpha_lo,
+                                                double& rn, bool& bad) {
+    const double acc = __dadd_rn(r, static_cast<double>(g));
+    const double aa = fabs(acc);
+    bad |= !(aa < __longlong_as_double(0x7ff0000000000000ll));
+    const bool nz = aa >= alpha;
+    const uint32_t ah = static_cast<uint32_t>(__double2hiint(acc));
+    const double sg = __hiloint2double(static_cast<int>(alpha_hi | (~ah & 0x80000000u)), static_cast<int>(alpha_lo));
+    const double t = __dadd_rn(acc, sg);
+    rn = nz ? t : acc;
+    return nz ? 1u + (ah >> 31) : 0u;
+}
+
 template <typename G>
 __global__ void __launch_bounds__(256) k_quantize(const G* __restrict__ g, const double* r_in,
                                                   double* r_out, uint32_t* __restrict__ words,
