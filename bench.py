@@ -46,6 +46,8 @@ def parse():
     ap.add_argument("--workload", default="resnet50", help="resnet50 | resnet20 | vgg16 | single:<n> | keys:a,b,..")
     ap.add_argument("--k", type=int, default=4)
     ap.add_argument("--alpha", type=float, default=0.5)
+    ap.add_argument("--exchange", choices=("p2p", "nccl"), default="p2p",
+                    help="p2p: all-gather fused into K1 over NVLink (symmetric memory); nccl: ncclAllGather")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="budget of the cpu_baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -152,20 +154,14 @@ def cpu_sample_layout(layout, budget_elems):
     return Layout(spans)
 
 
-def cpu_port_rounds(sizes, n_workers, k, alpha, rounds, seed=0, threads=None):
-    """Time `rounds` lock-step CD-SGD rounds of the CPU port; returns (seconds, kind, cores, impl)."""
-    from oracle import cpu_port
-
-    return cpu_port.time_rounds(sizes, n_workers, k, alpha, rounds, seed=seed, threads=threads)
-
-
 def cpu_baseline(layout, args, n_workers):
     from oracle import cpu_port
 
     sample = cpu_sample_layout(layout, 4_000_000)
-    # calibrate one round, then size the round count to the budget (whole k-periods)
-    t1, kind, cores, impl = cpu_port.time_rounds(sample.lengths, n_workers, args.k, args.alpha, 1)
-    rounds = max(args.k, int(args.cpu_seconds / max(t1, 1e-6)) // args.k * args.k)
+    # calibrate on one period (after an untimed warm-up round), then size the timed run to the
+    # budget in whole k-periods
+    tk, kind, cores, impl = cpu_port.time_rounds(sample.lengths, n_workers, args.k, args.alpha, args.k)
+    rounds = max(args.k, int(args.cpu_seconds / max(tk / args.k, 1e-6)) // args.k * args.k)
     secs, kind, cores, impl = cpu_port.time_rounds(sample.lengths, n_workers, args.k, args.alpha, rounds)
     value = n_workers * sample.total * rounds / secs / 1e9
     return {"value": value, "unit": UNIT, "cores": cores, "kind": kind,
@@ -185,13 +181,14 @@ def run_reference(args):
     layout = by_name(args.workload)
     n_workers = max(args.gpus, world)
     sample = cpu_sample_layout(layout, 2_000_000)
-    t1, kind, cores, impl = cpu_port.time_rounds(sample.lengths, n_workers, args.k, args.alpha, 1)
+    tk, kind, cores, impl = cpu_port.time_rounds(sample.lengths, n_workers, args.k, args.alpha, args.k)
+    t1 = tk / args.k
     # each step is a bounded sample sized so warmup+steps finish in ~2-3 minutes
     per_step_budget = 150.0 / max(1, args.steps + args.warmup)
     scale = max(0.05, min(1.0, per_step_budget / max(t1, 1e-6)))
     sample = cpu_sample_layout(layout, int(sample.total * scale))
-    cpu_port.time_rounds(sample.lengths, n_workers, args.k, args.alpha, args.warmup)
-    secs, kind, cores, impl = cpu_port.time_rounds(sample.lengths, n_workers, args.k, args.alpha, args.steps)
+    secs, kind, cores, impl = cpu_port.time_rounds(sample.lengths, n_workers, args.k, args.alpha, args.steps,
+                                                   warm=max(1, args.warmup))
     value = n_workers * sample.total * args.steps / secs / 1e9
     desc = (f"{args.steps} lock-step rounds x {n_workers} simulated workers on the first {len(sample)} keys "
             f"({sample.total:,} elements) of the {args.workload} layout; {impl}")
@@ -238,7 +235,7 @@ def run_ours(args):
     gen.manual_seed(1000 + rank)
     w0 = torch.randn(n, device=dev, generator=torch.Generator(device=dev).manual_seed(999))
     pool = [0.3 * torch.randn(n, device=dev, generator=gen) for _ in range(2)]
-    wk = CDSGDWorker(layout, hp, w0, rank=rank, comm=comm, gnorm_ring=64)
+    wk = CDSGDWorker(layout, hp, w0, rank=rank, comm=comm, gnorm_ring=64, exchange=args.exchange)
     stream = torch.cuda.current_stream(dev)
 
     def barrier():
@@ -366,7 +363,9 @@ def run_ours(args):
             "config": {"workload": workload_desc(layout, args.workload), "layout": args.workload,
                        "n_per_rank": n, "keys": len(layout), "k": args.k, "alpha": args.alpha, "algo": "cdsgd",
                        "warmup_n": 0, "residual": "fp64 (bit-exact)", "weights": "fp32",
-                       "exchange": "ncclAllGather(packed codes); ncclAllReduce(fp32) every k-th round",
+                       "exchange": ("codes all-gathered inside K1 by NVLink stores to peer memory (symmetric "
+                                    "memory, release/acquire flags)" if args.exchange == "p2p" and world > 1 else
+                                    "ncclAllGather(packed codes)") + "; ncclAllReduce(fp32) every k-th round",
                        "l2": f"inputs larger than L2: {(20 * n) / 2**20:.0f} MiB touched per step per rank",
                        "parallelism": f"dp{world}"},
             "roofline": roof, "kernels": kernels, "exchange": exch, "cpu_baseline": cpu, "e2e": e2e,

@@ -201,6 +201,16 @@ int cdsgd_engine_get_state(const cdsgd_engine* eng, cdsgd_engine_state* out);
 int cdsgd_engine_check(cdsgd_engine* eng, void* stream, int64_t* round, int64_t* index);
 /* 1 if round `t` (0-based) pushes codes under the engine's schedule (engine.py:345-355). */
 int cdsgd_engine_round_compressed(const cdsgd_engine* eng, int64_t t);
+/* Fused NVLink exchange (replaces the NCCL all-gather of codes on compressed rounds).
+ * Every rank allocates one symmetric buffer of cdsgd_p2p_bytes(nranks, words) bytes
+ * (zero-filled; e.g. torch symmetric memory), maps all peers' buffers, and passes
+ * the nranks base addresses (index = rank, 256-byte aligned) before round 0. K1 then
+ * stores each packed word directly into every rank's slot and publishes a release
+ * flag; K2 acquires all ranks' flags (spin on local memory, ~10 s timeout ->
+ * CDSGD_ERR_STATE at cdsgd_engine_check) and releases the slot. Correction rounds
+ * keep ncclAllReduce. Requires nranks <= 8 (one NVSwitch box). */
+int64_t cdsgd_p2p_bytes(int32_t nranks, int64_t words);
+int cdsgd_engine_attach_p2p(cdsgd_engine* eng, void* const* peer_bases, int32_t nranks);
 /* Make `stream` wait for every exchange the engine has issued so far. */
 int cdsgd_engine_join(cdsgd_engine* eng, void* stream);
 /* Per-kernel timing with CUDA events recorded on the launching streams around

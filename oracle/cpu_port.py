@@ -104,8 +104,8 @@ class CPortEngine:
         self.t += 1
 
 
-def time_rounds(sizes, n_workers, k, alpha, rounds, seed=0, threads=None):
-    """Run `rounds` lock-step rounds; returns (seconds, kind, cores, impl description)."""
+def time_rounds(sizes, n_workers, k, alpha, rounds, seed=0, threads=None, warm=1):
+    """Run `warm` untimed + `rounds` timed lock-step rounds; returns (seconds, kind, cores, impl)."""
     n = int(np.sum(sizes))
     rng = np.random.default_rng(seed)
     pool = [(0.3 * rng.standard_normal((n_workers, n))).astype(np.float32) for _ in range(2)]
@@ -115,15 +115,19 @@ def time_rounds(sizes, n_workers, k, alpha, rounds, seed=0, threads=None):
         if threads:
             lib.cdsgd_ref_set_threads(int(threads))
         eng = CPortEngine(w0, sizes, n_workers, k=k, alpha=alpha)
+        for r in range(warm):  # first touch of every buffer (page faults) stays out of the timing
+            eng.step(pool[r % 2])
         t0 = time.perf_counter()
         for r in range(rounds):
-            eng.step(pool[r % 2])
+            eng.step(pool[(warm + r) % 2])
         secs = time.perf_counter() - t0
         cores = lib.cdsgd_ref_threads()
         return secs, "port", cores, (f"C restatement of the reference NumPy round (oracle/cdsgd_oracle.c, "
                                      f"bit-identical), OpenMP {cores} threads")
     orc = O.LockstepOracle(w0, list(sizes), O.OracleHP("cdsgd", n_workers, 0.1, 0.4, k, alpha, 0))
+    for r in range(warm):
+        orc.step(list(pool[r % 2]))
     t0 = time.perf_counter()
     for r in range(rounds):
-        orc.step(list(pool[r % 2]))
+        orc.step(list(pool[(warm + r) % 2]))
     return time.perf_counter() - t0, "port", 1, "NumPy restatement (oracle/cdsgd_oracle.py), 1 thread"

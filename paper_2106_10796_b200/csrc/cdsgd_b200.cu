@@ -165,26 +165,26 @@ int launch_af_tma_cfg(const ApplyFArgs& a, cudaStream_t st) {
 }
 template <typename G, int WARPS, int ST>
 int launch_quant_tma(const G* g, const double* r_in, double* r_out, uint32_t* words, KeyTab kt, double alpha,
-                     uint64_t* err, uint64_t tag, cudaStream_t st) {
+                     uint64_t* err, uint64_t tag, cudaStream_t st, const P2PArgs& x) {
     using SM = QuantSmem<G, WARPS, ST>;
     static_assert(SM::BYTES <= 227 * 1024, "smem");
     if (!prepare_tma(k_quantize_tma<G, WARPS, ST>, SM::BYTES)) return fail(CDSGD_ERR_CUDA, "smem attribute");
     k_quantize_tma<G, WARPS, ST><<<tma_grid(kt.ntiles, WARPS), WARPS * 32, SM::BYTES, st>>>(g, r_in, r_out, words, kt,
-                                                                                          alpha, err, tag);
+                                                                                          alpha, err, tag, x);
     return CDSGD_OK;
 }
 template <typename G>
 int launch_quant_tma_cfg(const G* g, const double* r_in, double* r_out, uint32_t* words, KeyTab kt, double alpha,
-                         uint64_t* err, uint64_t tag, cudaStream_t st) {
+                         uint64_t* err, uint64_t tag, cudaStream_t st, const P2PArgs& x) {
     if constexpr (sizeof(G) == 8) {
-        return launch_quant_tma<G, 8, 3>(g, r_in, r_out, words, kt, alpha, err, tag, st);
+        return launch_quant_tma<G, 8, 3>(g, r_in, r_out, words, kt, alpha, err, tag, st, x);
     } else {
     switch (tma_cfg()) {
-        case 43: return launch_quant_tma<G, 4, 3>(g, r_in, r_out, words, kt, alpha, err, tag, st);
-        case 46: return launch_quant_tma<G, 4, 6>(g, r_in, r_out, words, kt, alpha, err, tag, st);
-        case 83: return launch_quant_tma<G, 8, 3>(g, r_in, r_out, words, kt, alpha, err, tag, st);
-        case 84: return launch_quant_tma<G, 8, 4>(g, r_in, r_out, words, kt, alpha, err, tag, st);
-        default: return launch_quant_tma<G, 16, 2>(g, r_in, r_out, words, kt, alpha, err, tag, st);
+        case 43: return launch_quant_tma<G, 4, 3>(g, r_in, r_out, words, kt, alpha, err, tag, st, x);
+        case 46: return launch_quant_tma<G, 4, 6>(g, r_in, r_out, words, kt, alpha, err, tag, st, x);
+        case 83: return launch_quant_tma<G, 8, 3>(g, r_in, r_out, words, kt, alpha, err, tag, st, x);
+        case 84: return launch_quant_tma<G, 8, 4>(g, r_in, r_out, words, kt, alpha, err, tag, st, x);
+        default: return launch_quant_tma<G, 16, 2>(g, r_in, r_out, words, kt, alpha, err, tag, st, x);
     }
     }
 }
@@ -277,10 +277,13 @@ extern "C" int cdsgd_quantize(const cdsgd_layout* L, const void* grad, int32_t g
     const KeyTab kt = L->tab();
     if (!use_ldg()) {
         int rc;
+        const P2PArgs nox{};
         if (gdt == CDSGD_F32)
-            rc = launch_quant_tma_cfg(static_cast<const float*>(grad), r_in, r_out, words, kt, alpha, err, tag, S(stream));
+            rc = launch_quant_tma_cfg(static_cast<const float*>(grad), r_in, r_out, words, kt, alpha, err, tag, S(stream),
+                                      nox);
         else if (gdt == CDSGD_F64)
-            rc = launch_quant_tma_cfg(static_cast<const double*>(grad), r_in, r_out, words, kt, alpha, err, tag, S(stream));
+            rc = launch_quant_tma_cfg(static_cast<const double*>(grad), r_in, r_out, words, kt, alpha, err, tag,
+                                      S(stream), nox);
         else
             return fail(CDSGD_ERR_ARG, "grad dtype must be CDSGD_F32 or CDSGD_F64");
         if (rc != CDSGD_OK) return rc;
@@ -415,7 +418,7 @@ inline bool pow2(int n) { return n > 0 && (n & (n - 1)) == 0; }
 int launch_apply_quant(const cdsgd_layout* L, float* W, const uint32_t* gathered, int nr, int64_t stride,
                        double alpha, double eta_g, const float* gnext, float* loc, double eta_l, uint64_t* err,
                        uint64_t skip_below, double* gnorm, const DecodeTab* tab_in, int exact_in,
-                       cudaStream_t st) {
+                       cudaStream_t st, const P2PArgs* x = nullptr) {
     if (L == nullptr) return fail(CDSGD_ERR_ARG, "layout is NULL");
     if (nr < 1 || nr > MAX_RANKS - 1) return fail(CDSGD_ERR_ARG, "nranks must be in [1, %d]", MAX_RANKS - 1);
     if ((gnext == nullptr) != (loc == nullptr)) return fail(CDSGD_ERR_ARG, "g_next and loc_out go together");
@@ -435,6 +438,7 @@ int launch_apply_quant(const cdsgd_layout* L, float* W, const uint32_t* gathered
     a.err = err;
     a.skip_below = skip_below;
     a.gnorm = gnorm;
+    a.x = x != nullptr ? *x : P2PArgs{};
     DecodeTab tab;
     int exact;
     if (tab_in != nullptr) {
@@ -450,7 +454,7 @@ int launch_apply_quant(const cdsgd_layout* L, float* W, const uint32_t* gathered
         const char* e = getenv("CDSGD_K2_TMA");
         return e != nullptr && e[0] == '1';
     }();
-    if (k2_tma && exact && nr <= 8) {
+    if (k2_tma && exact && nr <= 8 && a.x.nranks == 0) {
         int rc = CDSGD_OK;
 #define AQT(R)                                               \
     case R: rc = launch_aq_tma_cfg<R>(a, kt, tab, st); break;
@@ -593,6 +597,13 @@ struct cdsgd_engine {
     bool failed = false;
     int64_t err_base = 0;
     std::vector<int8_t> rlog;  // residual index at the entry of rounds err_base..t-1
+    // fused P2P exchange (symmetric memory): peer buffer bases and protocol state
+    bool p2p = false;
+    char* peer[MAX_RANKS_P2P] = {nullptr};
+    int64_t off_slot[2] = {0, 0}, off_ready = 0, off_freed = 0;
+    int64_t last_use[2] = {-1, -1};  // last compressed round that filled slot p
+    bool xused[2] = {false, false};  // round parity p used the NCCL stream
+    unsigned int* counters = nullptr;  // [2] grid-completion counters (K1, K2)
     // profiling: event pairs per kernel class (0 quant, 1 apply_q, 2 apply_f, 3 local, 4 exchange)
     bool prof = false;
     std::vector<cudaEvent_t> ev_pool;
@@ -641,7 +652,7 @@ int64_t words_of(const cdsgd_engine* E) { return E->L->nwords; }
 // the local update from g_next (nullable).
 int engine_apply(cdsgd_engine* E, int64_t p, bool comp, const float* gp, const float* gnext, cudaStream_t C) {
     const int nr = E->d.nranks;
-    if (nr > 1) CUDA_TRY(cudaStreamWaitEvent(C, E->evX[p & 1], 0));
+    if (nr > 1 && E->xused[p & 1]) CUDA_TRY(cudaStreamWaitEvent(C, E->evX[p & 1], 0));
     const int64_t rel = p - E->err_base + 1;
     const uint64_t skip_below = rel <= 0 ? 0ull : (static_cast<uint64_t>(rel) << CDSGD_INDEX_BITS);
     double* gn = nullptr;
@@ -651,10 +662,23 @@ int engine_apply(cdsgd_engine* E, int64_t p, bool comp, const float* gp, const f
     }
     float* loc = gnext ? E->d.loc : nullptr;
     if (comp) {
+        P2PArgs x{};
+        if (E->p2p) {
+            const int q = static_cast<int>(p & 1);
+            char* local = E->peer[E->d.rank];
+            x.nranks = nr;
+            for (int r = 0; r < nr; ++r)
+                x.publish[r] = reinterpret_cast<uint64_t*>(E->peer[r] + E->off_freed) + q * nr + E->d.rank;
+            x.wait_flags = reinterpret_cast<const uint64_t*>(local + E->off_ready) + q * nr;
+            x.wait_value = static_cast<uint64_t>(p) + 1;
+            x.publish_value = static_cast<uint64_t>(p) + 1;
+            x.counter = E->counters + 1;
+            x.err = E->d.err;
+        }
         const long pi = prof_start(E, 1, C);
         const int rc = launch_apply_quant(E->L, E->d.weights, E->d.gathered[p & 1], nr, words_of(E), E->d.alpha,
                                           E->d.eta_global, gnext, loc, E->d.eta_local, E->d.err, skip_below, gn,
-                                          &E->tab, E->exact, C);
+                                          &E->tab, E->exact, C, &x);
         prof_stop(E, pi, C);
         return rc;
     }
@@ -711,10 +735,53 @@ extern "C" int cdsgd_engine_create(const cdsgd_engine_desc* d, const cdsgd_layou
     return CDSGD_OK;
 }
 
+namespace {
+int64_t align256(int64_t v) { return (v + 255) & ~int64_t(255); }
+void p2p_offsets(int32_t nranks, int64_t words, int64_t* slot1, int64_t* ready, int64_t* freed, int64_t* total) {
+    const int64_t slot = align256(static_cast<int64_t>(nranks) * words * 4);
+    *slot1 = slot;
+    *ready = 2 * slot;
+    *freed = *ready + align256(2 * nranks * 8);
+    *total = *freed + align256(2 * nranks * 8);
+}
+}  // namespace
+
+extern "C" int64_t cdsgd_p2p_bytes(int32_t nranks, int64_t words) {
+    int64_t a, b, c, total;
+    p2p_offsets(nranks, words, &a, &b, &c, &total);
+    return total;
+}
+
+extern "C" int cdsgd_engine_attach_p2p(cdsgd_engine* E, void* const* peer_bases, int32_t nranks) {
+    if (E == nullptr || peer_bases == nullptr) return fail(CDSGD_ERR_ARG, "NULL argument");
+    if (nranks != E->d.nranks || nranks < 2) return fail(CDSGD_ERR_ARG, "attach_p2p needs nranks == workers >= 2");
+    if (nranks > MAX_RANKS_P2P) return fail(CDSGD_ERR_ARG, "fused exchange supports at most %d ranks", MAX_RANKS_P2P);
+    if (E->t != 0) return fail(CDSGD_ERR_STATE, "attach_p2p must precede the first round");
+    if (use_ldg()) return fail(CDSGD_ERR_ARG, "fused exchange needs the TMA quantizer (unset CDSGD_LDG)");
+    for (int r = 0; r < nranks; ++r) {
+        if (peer_bases[r] == nullptr || (reinterpret_cast<uintptr_t>(peer_bases[r]) & 255) != 0)
+            return fail(CDSGD_ERR_ARG, "peer base %d is NULL or not 256-byte aligned", r);
+        E->peer[r] = static_cast<char*>(peer_bases[r]);
+    }
+    int64_t total;
+    p2p_offsets(nranks, E->L->nwords, &E->off_slot[1], &E->off_ready, &E->off_freed, &total);
+    E->off_slot[0] = 0;
+    char* local = E->peer[E->d.rank];
+    E->d.gathered[0] = reinterpret_cast<uint32_t*>(local + E->off_slot[0]);
+    E->d.gathered[1] = reinterpret_cast<uint32_t*>(local + E->off_slot[1]);
+    if (E->counters == nullptr) {
+        CUDA_TRY(cudaMalloc(&E->counters, 2 * sizeof(unsigned int)));
+        CUDA_TRY(cudaMemset(E->counters, 0, 2 * sizeof(unsigned int)));
+    }
+    E->p2p = true;
+    return CDSGD_OK;
+}
+
 extern "C" int cdsgd_engine_join(cdsgd_engine* E, void* stream) {
     if (E == nullptr) return fail(CDSGD_ERR_ARG, "NULL engine");
     if (E->xs == nullptr || E->t == 0) return CDSGD_OK;
-    CUDA_TRY(cudaStreamWaitEvent(S(stream), E->evX[(E->t - 1) & 1], 0));
+    for (int64_t u = E->t - 1; u >= 0 && u >= E->t - 2; --u)
+        if (E->xused[u & 1]) CUDA_TRY(cudaStreamWaitEvent(S(stream), E->evX[u & 1], 0));
     return CDSGD_OK;
 }
 
@@ -751,6 +818,7 @@ extern "C" int cdsgd_engine_destroy(cdsgd_engine* E) {
         if (E->evX[i]) cudaEventDestroy(E->evX[i]);
     }
     if (E->xs) cudaStreamDestroy(E->xs);
+    if (E->counters) cudaFree(E->counters);
     delete E;
     return CDSGD_OK;
 }
@@ -779,14 +847,40 @@ extern "C" int cdsgd_engine_step(cdsgd_engine* E, const float* g, void* stream) 
     if (comp) {
         const uint64_t tag = static_cast<uint64_t>(t - E->err_base) << CDSGD_INDEX_BITS;
         const long pi = prof_start(E, 0, C);
-        rc = cdsgd_quantize(E->L, g, CDSGD_F32, E->d.residual[E->rcur], E->d.residual[E->rcur ^ 1], mine,
-                            E->d.alpha, E->d.err, tag, C);
+        if (E->p2p) {
+            // K1 with the all-gather fused in: words go straight into every rank's slot p
+            const int p = static_cast<int>(t & 1);
+            char* local = E->peer[E->d.rank];
+            P2PArgs x{};
+            x.nranks = nr;
+            for (int r = 0; r < nr; ++r) {
+                x.dst[r] = reinterpret_cast<uint32_t*>(E->peer[r] + E->off_slot[p]) + static_cast<int64_t>(E->d.rank) * nw;
+                x.publish[r] = reinterpret_cast<uint64_t*>(E->peer[r] + E->off_ready) + p * nr + E->d.rank;
+            }
+            x.wait_flags = reinterpret_cast<const uint64_t*>(local + E->off_freed) + p * nr;
+            x.wait_value = E->last_use[p] >= 0 ? static_cast<uint64_t>(E->last_use[p]) + 1 : 0;
+            x.publish_value = static_cast<uint64_t>(t) + 1;
+            x.counter = E->counters;
+            x.err = E->d.err;
+            rc = launch_quant_tma_cfg(g, E->d.residual[E->rcur], E->d.residual[E->rcur ^ 1], mine, E->L->tab(),
+                                      E->d.alpha, E->d.err, tag, C, x);
+            if (rc == CDSGD_OK) {
+                g_launches.fetch_add(1, std::memory_order_relaxed);
+                const cudaError_t le = cudaGetLastError();
+                if (le != cudaSuccess) rc = fail(CDSGD_ERR_CUDA, "kernel launch: %s", cudaGetErrorString(le));
+            }
+            E->last_use[p] = t;
+        } else {
+            rc = cdsgd_quantize(E->L, g, CDSGD_F32, E->d.residual[E->rcur], E->d.residual[E->rcur ^ 1], mine,
+                                E->d.alpha, E->d.err, tag, C);
+        }
         prof_stop(E, pi, C);
         if (rc != CDSGD_OK) return rc;
         E->rcur ^= 1;
     }
-    // 2. exchange round t on the engine's stream
-    if (nr > 1) {
+    // 2. exchange round t on the engine's stream (codes are already delivered when fused)
+    E->xused[t & 1] = nr > 1 && !(comp && E->p2p);
+    if (E->xused[t & 1]) {
         CUDA_TRY(cudaEventRecord(E->evQ[t & 1], C));
         CUDA_TRY(cudaStreamWaitEvent(E->xs, E->evQ[t & 1], 0));
         const long pi = prof_start(E, 4, E->xs);
@@ -871,6 +965,10 @@ extern "C" int cdsgd_engine_check(cdsgd_engine* E, void* stream, int64_t* round,
         E->failed = true;
         return fail(CDSGD_ERR_NUMERIC, "non-finite accumulated gradient at round %lld, element %lld",
                     (long long)s, (long long)idx);
+    }
+    if (h[1] == EXCHANGE_TIMEOUT) {
+        E->failed = true;
+        return fail(CDSGD_ERR_STATE, "fused exchange timed out waiting for a peer (lost rank?)");
     }
     if (h[1] != NO_ERR) {
         if (index) *index = static_cast<int64_t>(h[1]);

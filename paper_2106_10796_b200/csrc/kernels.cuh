@@ -28,6 +28,7 @@ constexpr int TILE_WORDS = 32;
 constexpr int TILE_ELEMS = 512;
 constexpr int CHUNKS = 4;           // 128-element chunks per tile (fast path)
 constexpr uint64_t NO_ERR = ~0ull;
+constexpr int MAX_RANKS_P2P = 8;  // fused NVLink exchange: one box of <= 8 GPUs
 
 struct KeyTab {
     const int64_t* eoff;  // [nkeys+1] element offsets
@@ -145,6 +146,70 @@ __device__ __forceinline__ uint64_t warp_min_u64(uint64_t v) {
         v = u < v ? u : v;
     }
     return v;
+}
+
+// ================================================================ peer exchange (P2P over NVLink)
+// Fused exchange protocol (see cdsgd_b200.cu, engine): K1 of round t stores every
+// packed word straight into each peer's gathered slot (NVLink stores through
+// symmetric-memory mappings) and the last CTA publishes ready[slot][me] = t+1 on
+// every peer with a system-scope release; K2 acquires ready[slot][*] >= t+1 before
+// reading and finally publishes freed[slot][me] = t+1 so producers may reuse the
+// slot. Waits spin on LOCAL memory with a timeout: on expiry the kernel records
+// EXCHANGE_TIMEOUT in err[1] and continues, so a lost peer can never hang the GPU.
+constexpr uint64_t EXCHANGE_TIMEOUT = 0xFFFFFFFFFFFFFFFEull;
+struct P2PArgs {
+    uint32_t* dst[MAX_RANKS_P2P];       // per rank r: where my words land in r's slot (nullptr = none)
+    uint64_t* publish[MAX_RANKS_P2P];   // per rank r: my flag cell in r's memory
+    const uint64_t* wait_flags;         // local flags [nranks] to wait on (nullptr = no wait)
+    uint64_t wait_value;
+    uint64_t publish_value;
+    unsigned int* counter;              // local grid-completion counter (0 between launches)
+    uint64_t* err;                      // err[1] receives EXCHANGE_TIMEOUT
+    int nranks;                         // 0: exchange disabled
+};
+
+__device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* p) {
+    uint64_t v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_sys(uint64_t* p, uint64_t v) {
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// Block-wide: thread 0 waits until every wait_flags[r] >= wait_value, then all threads proceed.
+__device__ __forceinline__ void p2p_wait(const P2PArgs& x) {
+    if (x.nranks > 0 && x.wait_flags != nullptr && x.wait_value != 0) {
+        if (threadIdx.x == 0) {
+            const long long t0 = clock64();
+            for (int r = 0; r < x.nranks; ++r) {
+                while (ld_acquire_sys(x.wait_flags + r) < x.wait_value) {
+                    __nanosleep(64);
+                    if (clock64() - t0 > (20ll << 30)) {  // ~10 s at 2 GHz
+                        if (x.err) atomicExch(reinterpret_cast<unsigned long long*>(x.err + 1), EXCHANGE_TIMEOUT);
+                        break;
+                    }
+                }
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// Block-wide epilogue: the last CTA to finish publishes publish_value to every peer.
+__device__ __forceinline__ void p2p_publish(const P2PArgs& x) {
+    if (x.nranks <= 0) return;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence_system();
+        const unsigned prev = atomicAdd(x.counter, 1u);
+        if (prev == gridDim.x - 1) {
+            __threadfence_system();
+            *x.counter = 0u;
+            for (int r = 0; r < x.nranks; ++r)
+                if (x.publish[r] != nullptr) st_release_sys(x.publish[r], x.publish_value);
+        }
+    }
 }
 
 // ================================================================ K1: quantize
@@ -326,6 +391,7 @@ struct ApplyQArgs {
     uint64_t* err;
     uint64_t skip_below;
     double* gnorm;
+    P2PArgs x;  // fused exchange: wait for peers' codes, then release the slot
 };
 
 __device__ __forceinline__ double apply_mean_general(const uint32_t* codes, int nr, double alpha,
@@ -342,7 +408,8 @@ __device__ __forceinline__ double apply_mean_general(const uint32_t* codes, int 
 
 template <int NR>  // NR > 0: compile-time rank count; NR == 0: runtime (generic)
 __global__ void __launch_bounds__(256) k_apply_quant(ApplyQArgs a, KeyTab kt, DecodeTab tab) {
-    if (a.err != nullptr && *reinterpret_cast<volatile uint64_t*>(a.err) < a.skip_below) return;
+    p2p_wait(a.x);
+    const bool skip = a.err != nullptr && *reinterpret_cast<volatile uint64_t*>(a.err) < a.skip_below;
     __shared__ double s_mean[2 * MAX_RANKS + 1];
     __shared__ float s_upd[2 * MAX_RANKS + 1];
     const int nr = NR > 0 ? NR : a.nranks;
@@ -357,7 +424,7 @@ __global__ void __launch_bounds__(256) k_apply_quant(ApplyQArgs a, KeyTab kt, De
     double gsq = 0.0;
     uint64_t bad_idx = NO_ERR;
     const bool do_loc = a.loc != nullptr;
-    if (tb < te) {
+    if (tb < te && !skip) {
         TileCursor kc;
         kc.seek(kt, tb);
         for (int64_t ti = tb; ti < te; ++ti) {
@@ -460,6 +527,7 @@ __global__ void __launch_bounds__(256) k_apply_quant(ApplyQArgs a, KeyTab kt, De
         if (lane == 0 && bad_idx != NO_ERR)
             atomicMin(reinterpret_cast<unsigned long long*>(a.err + 1), static_cast<unsigned long long>(bad_idx));
     }
+    p2p_publish(a.x);
 }
 
 // ================================================================ dequantize / aggregate

@@ -103,17 +103,20 @@ struct QuantSmem {
 template <typename G, int WARPS, int S>
 __global__ void __launch_bounds__(WARPS * 32, 1)
     k_quantize_tma(const G* __restrict__ g, const double* r_in, double* r_out, uint32_t* __restrict__ words,
-                   KeyTab kt, double alpha, uint64_t* err, uint64_t tag) {
+                   KeyTab kt, double alpha, uint64_t* err, uint64_t tag, P2PArgs x) {
     using SM = QuantSmem<G, WARPS, S>;
     extern __shared__ __align__(128) unsigned char smem[];
-    if (err != nullptr && *reinterpret_cast<volatile uint64_t*>(err) != NO_ERR) return;
+    p2p_wait(x);  // fused exchange: peers have released the slot we are about to fill
+    const bool aborted = err != nullptr && *reinterpret_cast<volatile uint64_t*>(err) != NO_ERR;
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     unsigned char* ring = smem + warp * SM::WARP;
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + WARPS * SM::WARP) + warp * S;
     int64_t tb, te;
     warp_range(kt.ntiles, tb, te);
-    if (tb >= te) return;
+    if (aborted) te = tb;  // sticky abort: no work, but still take part in the exchange protocol
+    uint64_t bad_idx = NO_ERR;
+    if (tb < te) {
     if (lane == 0) {
         for (int s = 0; s < S; ++s) tma::mbar_init(&bars[s], 1);
         tma::fence_mbar_init();
@@ -141,7 +144,6 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
         }
     };
     for (int i = 0; i < S - 1 && tb + i < te; ++i) issue(tb + i, i);
-    uint64_t bad_idx = NO_ERR;
     int slot = 0;
     for (int64_t ti = tb; ti < te; ++ti) {
         if (ti + S - 1 < te) {
@@ -219,14 +221,23 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
                 if (lane == 2 * s + 1) myword = interleave_codes(pm >> 16, mm >> 16);
             }
         }
-        if (lane < nw) words[w0 + lane] = myword;
+        if (lane < nw) {
+            if (x.nranks > 0) {
+                // fused all-gather: the word goes straight into every rank's slot (NVLink stores)
+                for (int r = 0; r < x.nranks; ++r) x.dst[r][w0 + lane] = myword;
+            } else {
+                words[w0 + lane] = myword;
+            }
+        }
         slot = slot + 1 == S ? 0 : slot + 1;
     }
+    }  // tb < te
     if (err != nullptr) {
         bad_idx = warp_min_u64(bad_idx);
         if (lane == 0 && bad_idx != NO_ERR)
             atomicMin(reinterpret_cast<unsigned long long*>(err), static_cast<unsigned long long>(bad_idx));
     }
+    p2p_publish(x);
 }
 
 // ================================================================ K2 (TMA)

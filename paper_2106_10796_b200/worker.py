@@ -49,6 +49,8 @@ class CDSGDWorker:
         gnorm_ring: int = 64,
         check_every: int = 0,
         device=None,
+        exchange: str = "p2p",
+        group=None,
     ):
         if not torch.cuda.is_available():
             raise _lib.LibraryError("CDSGDWorker needs a CUDA device (no CPU fallback)")
@@ -107,10 +109,36 @@ class CDSGDWorker:
                 "cdsgd_engine_create",
             )
             self._eng = out
+            self.exchange = exchange if self.world > 1 else "local"
+            if self.world > 1 and exchange == "p2p":
+                self._attach_p2p(group)
+            elif self.world > 1 and exchange != "nccl":
+                raise ConfigError(f"exchange must be 'p2p' or 'nccl', got {exchange!r}")
         self._keep: list[torch.Tensor] = []  # gradients still read by in-flight rounds
         self.check_every = int(check_every)
         self._since_check = 0
         self._lib = _lib.lib()
+
+    def _attach_p2p(self, group) -> None:
+        """Fused NVLink exchange: one symmetric buffer per rank (torch symmetric memory maps
+        every peer's buffer into this process); K1 stores codes straight into all ranks'
+        slots and K2 synchronises on release/acquire flags (cdsgd_engine_attach_p2p)."""
+        import torch.distributed as dist
+        import torch.distributed._symmetric_memory as symm_mem
+
+        lib = _lib.lib()
+        nbytes = int(lib.cdsgd_p2p_bytes(self.world, self.layout.n_words))
+        grp = group if group is not None else dist.group.WORLD
+        self._symm = symm_mem.empty(nbytes, dtype=torch.uint8, device=self.device)
+        self._symm.zero_()
+        torch.cuda.synchronize(self.device)
+        self._symm_handle = symm_mem.rendezvous(self._symm, grp)
+        ptrs = [int(p) for p in self._symm_handle.buffer_ptrs]
+        if len(ptrs) != self.world:
+            raise ConfigError("symmetric memory group does not match hp.workers")
+        arr = (C.c_void_p * self.world)(*ptrs)
+        _lib.check(lib.cdsgd_engine_attach_p2p(self._eng, arr, self.world), "cdsgd_engine_attach_p2p")
+        dist.barrier(group=grp)  # every rank's flags are zero before any rank's first K1
 
     # ------------------------------------------------------------------ state
     def state(self) -> _lib.EngineState:

@@ -9,7 +9,7 @@ for N in 1 2 4 8; do
   if [ $N -eq 1 ]; then
     timeout 300 python bench.py --steps 40 --warmup 10 --no-cpu-baseline > gpurun_out/bench_n$N.log 2>&1
   else
-    timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 --master-port 29531 bench.py --gpus $N --steps 40 --warmup 10 > gpurun_out/bench_n$N.log 2>&1
+    timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 --master-port 29531 bench.py --gpus $N --steps 40 --warmup 10 $EXTRA > gpurun_out/bench_n$N.log 2>&1
   fi
   echo "bench N=$N rc=$?"
   python - $N <<'PY'

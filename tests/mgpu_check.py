@@ -41,6 +41,36 @@ CASES = [
 ]
 
 
+def run_case(case, exchange, comm, rank, world, dev):
+    algo, sizes, k, warm, iters, alpha = case
+    layout = Layout.from_lengths(sizes)
+    n = layout.total
+    hp = HyperParams(algo=algo, workers=world, eta_global=0.1, eta_local=0.4, k=k, alpha=alpha, warmup_n=warm)
+    w0 = O.synthetic_weights(5, n)
+    wk = CDSGDWorker(layout, hp, w0, rank=rank, comm=comm, exchange=exchange)
+    orc = O.LockstepOracle(w0.astype(np.float64), sizes, O.OracleHP(algo, world, 0.1, 0.4, k, alpha, warm))
+    tag = f"{exchange}/{algo} rank {rank}"
+    for t in range(iters):
+        np.testing.assert_allclose(wk.compute_weights().cpu().numpy(), orc.compute_weights(rank), rtol=RTOL,
+                                   atol=ATOL, err_msg=f"{tag} compute weights round {t}")
+        grads = [O.synthetic_grad(5, t, w, n) for w in range(world)]
+        wk.step(torch.from_numpy(grads[rank]).to(dev))
+        orc.step(grads)
+        res = wk.residual.cpu().numpy()
+        assert np.array_equal(res.view(np.uint64), orc.workers[rank].residual.view(np.uint64)), \
+            f"{tag} residual round {t}"
+    wk.flush()
+    W = wk.weights
+    np.testing.assert_allclose(W.cpu().numpy(), orc.W, rtol=RTOL, atol=ATOL, err_msg=f"{tag} W")
+    allW = [torch.empty_like(W) for _ in range(world)]
+    dist.all_gather(allW, W)
+    for w in range(world):
+        assert torch.equal(allW[w], W), f"{tag}: W replica of rank {w} differs"
+    for t in range(iters):
+        assert abs(wk.grad_norm(t) - orc.grad_norms[t]) <= 1e-5 * max(1.0, orc.grad_norms[t]), (tag, t)
+    wk.close()
+
+
 def main():
     rank, world, local = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"]), int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
@@ -48,36 +78,14 @@ def main():
     dist.init_process_group("nccl", device_id=dev)
     _lib.load()
     comm = Comm(share_unique_id(rank), world, rank)
-    for algo, sizes, k, warm, iters, alpha in CASES:
-        layout = Layout.from_lengths(sizes)
-        n = layout.total
-        hp = HyperParams(algo=algo, workers=world, eta_global=0.1, eta_local=0.4, k=k, alpha=alpha, warmup_n=warm)
-        w0 = O.synthetic_weights(5, n)
-        wk = CDSGDWorker(layout, hp, w0, rank=rank, comm=comm)
-        orc = O.LockstepOracle(w0.astype(np.float64), sizes, O.OracleHP(algo, world, 0.1, 0.4, k, alpha, warm))
-        for t in range(iters):
-            np.testing.assert_allclose(wk.compute_weights().cpu().numpy(), orc.compute_weights(rank), rtol=RTOL,
-                                       atol=ATOL, err_msg=f"{algo} rank {rank} compute weights round {t}")
-            grads = [O.synthetic_grad(5, t, w, n) for w in range(world)]
-            wk.step(torch.from_numpy(grads[rank]).to(dev))
-            orc.step(grads)
-            res = wk.residual.cpu().numpy()
-            assert np.array_equal(res.view(np.uint64), orc.workers[rank].residual.view(np.uint64)), \
-                f"{algo} rank {rank} residual round {t}"
-        wk.flush()
-        W = wk.weights
-        np.testing.assert_allclose(W.cpu().numpy(), orc.W, rtol=RTOL, atol=ATOL, err_msg=f"{algo} rank {rank} W")
-        allW = [torch.empty_like(W) for _ in range(world)]
-        dist.all_gather(allW, W)
-        for w in range(world):
-            assert torch.equal(allW[w], W), f"{algo}: W replica of rank {w} differs from rank {rank}"
-        for t in range(iters):
-            assert abs(wk.grad_norm(t) - orc.grad_norms[t]) <= 1e-5 * max(1.0, orc.grad_norms[t]), (algo, t)
-        wk.close()
+    exchanges = sys.argv[1:] or ["p2p", "nccl"]
+    for exchange in exchanges:
+        for case in CASES:
+            run_case(case, exchange, comm, rank, world, dev)
     comm.close()
     dist.barrier(device_ids=[local])
     if rank == 0:
-        print(f"MGPU OK world={world} cases={len(CASES)}", flush=True)
+        print(f"MGPU OK world={world} cases={len(CASES)} exchanges={exchanges}", flush=True)
     dist.destroy_process_group()
 
 
