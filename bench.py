@@ -282,6 +282,8 @@ def run_ours(args):
         "apply_quant": 4 * n + 4 * n + 4 * n + 4 * n + world * 4 * nw,
         "apply_full": 5 * 4 * n,
         "local_update": 3 * 4 * n,
+        # apply(t-1) + quantize(t): g 4 | r 8+8 | W 4+4 | loc 4 | codes in N/4 + out 1/4
+        "fused": 4 * n + 16 * n + 8 * n + 4 * n + world * 4 * nw + 4 * nw,
     }
     kernels = {}
     for kname, nbytes in alg.items():

@@ -215,11 +215,12 @@ int cdsgd_engine_attach_p2p(cdsgd_engine* eng, void* const* peer_bases, int32_t 
 int cdsgd_engine_join(cdsgd_engine* eng, void* stream);
 /* Per-kernel timing with CUDA events recorded on the launching streams around
  * each K1 / K2 / K3 / local-update launch and each NCCL call, between _begin and
- * _end. _end synchronises and writes 10 doubles:
+ * _end. _end synchronises and writes 12 doubles:
  * {quant_ms, quant_n, apply_quant_ms, apply_quant_n, apply_full_ms, apply_full_n,
- *  local_ms, local_n, exchange_ms, exchange_n} (ms are sums over launches). */
+ *  local_ms, local_n, exchange_ms, exchange_n, fused_ms, fused_n} (ms are sums over
+ * launches; "fused" = apply(t-1) + quantize(t) in one kernel). */
 int cdsgd_engine_profile_begin(cdsgd_engine* eng);
-int cdsgd_engine_profile_end(cdsgd_engine* eng, double* out10);
+int cdsgd_engine_profile_end(cdsgd_engine* eng, double* out12);
 
 #ifdef __cplusplus
 }

@@ -40,7 +40,7 @@ def sources():
 
 
 def deps():
-    return sources() + [os.path.join(CSRC, "kernels.cuh"), os.path.join(CSRC, "kernels_tma.cuh"), os.path.join(INCLUDE, "cdsgd_b200.h")]
+    return sources() + [os.path.join(CSRC, "kernels.cuh"), os.path.join(CSRC, "kernels_tma.cuh"), os.path.join(CSRC, "kernels_fused.cuh"), os.path.join(INCLUDE, "cdsgd_b200.h")]
 
 
 def up_to_date() -> bool:

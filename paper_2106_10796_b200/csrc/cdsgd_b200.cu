@@ -15,6 +15,7 @@
 #include "cdsgd_b200.h"
 #include "kernels.cuh"
 #include "kernels_tma.cuh"
+#include "kernels_fused.cuh"
 
 using namespace cdsgd;
 
@@ -506,6 +507,52 @@ int launch_apply_full(float* W, const float* gsum, int nr, int64_t n, double eta
     LAUNCH_CHECK();
     return CDSGD_OK;
 }
+// Fused apply(t-1) + quantize(t). CDSGD_FUSED_CFG=<warps>x<stages> (default 12x2).
+int fused_cfg() {
+    static const int v = read_cfg("CDSGD_FUSED_CFG", 122);
+    return v;
+}
+template <int NR, int AP, int WP, int ST>
+int launch_fused_t(const FusedArgs& a, const KeyTab& kt, const DecodeTab& tab, cudaStream_t st) {
+    using SM = FusedSmem<NR, AP, WP, ST>;
+    if constexpr (SM::BYTES > 227 * 1024) {
+        return launch_fused_t<NR, AP, 8, 2>(a, kt, tab, st);  // configuration does not fit: default
+    }
+    if (!prepare_tma(k_fused<NR, AP, WP, ST>, SM::BYTES)) return fail(CDSGD_ERR_CUDA, "smem attribute");
+    k_fused<NR, AP, WP, ST><<<tma_grid(kt.ntiles, WP), WP * 32, SM::BYTES, st>>>(a, kt, tab);
+    return CDSGD_OK;
+}
+template <int NR, int AP>
+int launch_fused_cfg(const FusedArgs& a, const KeyTab& kt, const DecodeTab& tab, cudaStream_t st) {
+    switch (fused_cfg()) {
+        case 82: return launch_fused_t<NR, AP, 8, 2>(a, kt, tab, st);
+        case 62: return launch_fused_t<NR, AP, 6, 2>(a, kt, tab, st);
+        case 83: return launch_fused_t<NR, AP, 8, 3>(a, kt, tab, st);
+        default: return launch_fused_t<NR, AP, 12, 2>(a, kt, tab, st);
+    }
+}
+int launch_fused(int nr, bool apply_quant, const FusedArgs& a, const KeyTab& kt, const DecodeTab& tab,
+                 cudaStream_t st) {
+    int rc;
+    if (!apply_quant) {
+        rc = launch_fused_cfg<1, APPLY_F>(a, kt, tab, st);
+    } else {
+        switch (nr) {
+            case 1: rc = launch_fused_cfg<1, APPLY_Q>(a, kt, tab, st); break;
+            case 2: rc = launch_fused_cfg<2, APPLY_Q>(a, kt, tab, st); break;
+            case 3: rc = launch_fused_cfg<3, APPLY_Q>(a, kt, tab, st); break;
+            case 4: rc = launch_fused_cfg<4, APPLY_Q>(a, kt, tab, st); break;
+            case 5: rc = launch_fused_cfg<5, APPLY_Q>(a, kt, tab, st); break;
+            case 6: rc = launch_fused_cfg<6, APPLY_Q>(a, kt, tab, st); break;
+            case 7: rc = launch_fused_cfg<7, APPLY_Q>(a, kt, tab, st); break;
+            case 8: rc = launch_fused_cfg<8, APPLY_Q>(a, kt, tab, st); break;
+            default: return fail(CDSGD_ERR_ARG, "fused step supports 1..8 ranks");
+        }
+    }
+    if (rc != CDSGD_OK) return rc;
+    LAUNCH_CHECK();
+    return CDSGD_OK;
+}
 }  // namespace
 
 extern "C" int cdsgd_apply_quant(const cdsgd_layout* L, float* W, const uint32_t* gathered, int32_t nr,
@@ -603,8 +650,9 @@ struct cdsgd_engine {
     int64_t off_slot[2] = {0, 0}, off_ready = 0, off_freed = 0;
     int64_t last_use[2] = {-1, -1};  // last compressed round that filled slot p
     bool xused[2] = {false, false};  // round parity p used the NCCL stream
-    unsigned int* counters = nullptr;  // [2] grid-completion counters (K1, K2)
-    // profiling: event pairs per kernel class (0 quant, 1 apply_q, 2 apply_f, 3 local, 4 exchange)
+    unsigned int* counters = nullptr;  // [2] grid-completion counters (K1/fused, K2)
+    bool fuse = false;                 // apply(t-1) + quantize(t) in one kernel (N=1 or P2P)
+    // profiling: event pairs per kernel class (0 quant, 1 apply_q, 2 apply_f, 3 local, 4 exchange, 5 fused)
     bool prof = false;
     std::vector<cudaEvent_t> ev_pool;
     size_t ev_used = 0;
@@ -717,6 +765,10 @@ extern "C" int cdsgd_engine_create(const cdsgd_engine_desc* d, const cdsgd_layou
     E->exact = alpha_exact(d->alpha, d->nranks) ? 1 : 0;
     build_tab(E->tab, d->alpha, d->eta_global, d->nranks);
     E->compute_is_loc = E->uses_local && E->n_warmup == 0;
+    {
+        const char* nf = getenv("CDSGD_NO_FUSE");
+        E->fuse = d->nranks == 1 && !(nf != nullptr && nf[0] == '1') && !use_ldg();
+    }
     cudaError_t e = cudaSuccess;
     if (d->nranks > 1) {
         int lo = 0, hi = 0;
@@ -774,6 +826,10 @@ extern "C" int cdsgd_engine_attach_p2p(cdsgd_engine* E, void* const* peer_bases,
         CUDA_TRY(cudaMemset(E->counters, 0, 2 * sizeof(unsigned int)));
     }
     E->p2p = true;
+    {
+        const char* nf = getenv("CDSGD_NO_FUSE");
+        E->fuse = !(nf != nullptr && nf[0] == '1');
+    }
     return CDSGD_OK;
 }
 
@@ -796,7 +852,7 @@ extern "C" int cdsgd_engine_profile_begin(cdsgd_engine* E) {
 extern "C" int cdsgd_engine_profile_end(cdsgd_engine* E, double* out) {
     if (E == nullptr || out == nullptr) return fail(CDSGD_ERR_ARG, "NULL argument");
     E->prof = false;
-    for (int i = 0; i < 10; ++i) out[i] = 0.0;
+    for (int i = 0; i < 12; ++i) out[i] = 0.0;
     for (const auto& m : E->prof_marks) {
         CUDA_TRY(cudaEventSynchronize(E->ev_pool[m.second + 1]));
         float ms = 0.f;
@@ -842,6 +898,68 @@ extern "C" int cdsgd_engine_step(cdsgd_engine* E, const float* g, void* stream) 
     const int nr = E->d.nranks;
     const int64_t nw = words_of(E);
     uint32_t* mine = E->d.gathered[t & 1] + static_cast<int64_t>(E->d.rank) * nw;
+    const bool sync_path0 = !E->uses_local || t < E->n_warmup - 1;
+    if (E->fuse && comp && E->pending && !sync_path0 && (E->pend_comp || nr == 1)) {
+        // ---- one kernel: apply(t-1) fused with quantize(t); both read g_t once
+        const int64_t pnd = E->pend_t;
+        FusedArgs a{};
+        a.g = g;
+        a.r_in = E->d.residual[E->rcur];
+        a.r_out = E->d.residual[E->rcur ^ 1];
+        a.words = mine;
+        a.alpha = E->d.alpha;
+        a.tag = static_cast<uint64_t>(t - E->err_base) << CDSGD_INDEX_BITS;
+        a.W = E->d.weights;
+        a.loc = E->d.loc;
+        a.gathered = E->d.gathered[pnd & 1];
+        a.stride = nw;
+        a.gsum = E->pend_grad;  // N=1 correction round: the mean is g_{t-1} itself
+        a.scale = static_cast<float>(E->d.eta_global / nr);
+        a.inv_n = 1.0 / nr;
+        a.eta_l = static_cast<float>(E->d.eta_local);
+        const int64_t rel = pnd - E->err_base + 1;
+        a.skip_below = rel <= 0 ? 0ull : (static_cast<uint64_t>(rel) << CDSGD_INDEX_BITS);
+        a.err = E->d.err;
+        if (E->d.gnorm_sq != nullptr && E->d.gnorm_ring > 0) {
+            a.gnorm = E->d.gnorm_sq + (pnd % E->d.gnorm_ring);
+            CUDA_TRY(cudaMemsetAsync(a.gnorm, 0, sizeof(double), C));
+        }
+        if (E->p2p) {
+            const int p = static_cast<int>(t & 1), q = static_cast<int>(pnd & 1);
+            char* local = E->peer[E->d.rank];
+            a.xq.nranks = a.xa.nranks = nr;
+            for (int r = 0; r < nr; ++r) {
+                a.xq.dst[r] = reinterpret_cast<uint32_t*>(E->peer[r] + E->off_slot[p]) + static_cast<int64_t>(E->d.rank) * nw;
+                a.xq.publish[r] = reinterpret_cast<uint64_t*>(E->peer[r] + E->off_ready) + p * nr + E->d.rank;
+                a.xa.publish[r] = reinterpret_cast<uint64_t*>(E->peer[r] + E->off_freed) + q * nr + E->d.rank;
+            }
+            a.xq.wait_flags = reinterpret_cast<const uint64_t*>(local + E->off_freed) + p * nr;
+            a.xq.wait_value = E->last_use[p] >= 0 ? static_cast<uint64_t>(E->last_use[p]) + 1 : 0;
+            a.xq.publish_value = static_cast<uint64_t>(t) + 1;
+            a.xq.counter = E->counters;
+            a.xq.err = E->d.err;
+            a.xa.wait_flags = reinterpret_cast<const uint64_t*>(local + E->off_ready) + q * nr;
+            a.xa.wait_value = static_cast<uint64_t>(pnd) + 1;
+            a.xa.publish_value = static_cast<uint64_t>(pnd) + 1;
+            a.xa.counter = E->counters;
+            a.xa.err = E->d.err;
+            E->last_use[p] = t;
+        }
+        E->rlog.push_back(static_cast<int8_t>(E->rcur));
+        const long pi = prof_start(E, 5, C);
+        rc = launch_fused(nr, E->pend_comp, a, E->L->tab(), E->tab, C);
+        prof_stop(E, pi, C);
+        if (rc != CDSGD_OK) return rc;
+        E->rcur ^= 1;
+        E->xused[t & 1] = false;
+        E->pending = true;
+        E->pend_t = t;
+        E->pend_comp = true;
+        E->pend_grad = g;
+        E->compute_is_loc = true;
+        E->t = t + 1;
+        return CDSGD_OK;
+    }
     // 1. this round's contribution (K1 on compressed rounds)
     E->rlog.push_back(static_cast<int8_t>(E->rcur));
     if (comp) {
