@@ -413,6 +413,7 @@ void build_tab(DecodeTab& tab, double alpha, double eta_g, int nr) {
         tab.mean[c + nr] = mean;
         tab.upd[c + nr] = static_cast<float>(eta_g * mean);           // engine.py:511 (eta*mean)
     }
+    tab.sq_scale = (alpha / nr) * (alpha / nr);
 }
 inline bool pow2(int n) { return n > 0 && (n & (n - 1)) == 0; }
 
@@ -507,9 +508,13 @@ int launch_apply_full(float* W, const float* gsum, int nr, int64_t n, double eta
     LAUNCH_CHECK();
     return CDSGD_OK;
 }
-// Fused apply(t-1) + quantize(t). CDSGD_FUSED_CFG=<warps>x<stages> (default 12x2).
-int fused_cfg() {
-    static const int v = read_cfg("CDSGD_FUSED_CFG", 122);
+// Fused apply(t-1) + quantize(t): LDG variant by default (measured faster than the TMA ring).
+int fused_cfg() {  // 0 (default) = register-staged LDG variant; <warps>x<stages> = TMA ring variant
+    static const int v = [] {
+        const char* e = getenv("CDSGD_FUSED_CFG");
+        if (e == nullptr || strcmp(e, "ldg") == 0) return 0;
+        return read_cfg("CDSGD_FUSED_CFG", 122);
+    }();
     return v;
 }
 template <int NR, int AP, int WP, int ST>
@@ -524,6 +529,10 @@ int launch_fused_t(const FusedArgs& a, const KeyTab& kt, const DecodeTab& tab, c
 }
 template <int NR, int AP>
 int launch_fused_cfg(const FusedArgs& a, const KeyTab& kt, const DecodeTab& tab, cudaStream_t st) {
+    if (fused_cfg() == 0) {  // CDSGD_FUSED_CFG=ldg: register-staged variant, 2 CTAs/SM
+        k_fused_ldg<NR, AP><<<tile_grid(k_fused_ldg<NR, AP>, kt.ntiles), THREADS, 0, st>>>(a, kt, tab);
+        return CDSGD_OK;
+    }
     switch (fused_cfg()) {
         case 82: return launch_fused_t<NR, AP, 8, 2>(a, kt, tab, st);
         case 62: return launch_fused_t<NR, AP, 6, 2>(a, kt, tab, st);

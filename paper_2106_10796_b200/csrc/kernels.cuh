@@ -348,6 +348,7 @@ constexpr int MAX_RANKS = 16;
 struct DecodeTab {
     double mean[2 * MAX_RANKS + 1];  // (cnt*alpha)/N
     float upd[2 * MAX_RANKS + 1];    // (float)(eta_g * mean)
+    double sq_scale;                 // (alpha/N)^2: grad-norm metric from integer sum(cnt^2)
 };
 
 // Counts over ranks for the 16 codes of one word position: returns packed 4-bit
@@ -369,6 +370,16 @@ __device__ __forceinline__ int count_at(const Counts& c, int j) {
     const uint32_t p = (j & 1) ? c.po : c.pe;
     const uint32_t m = (j & 1) ? c.mo : c.me;
     return static_cast<int>((p >> sh) & 15u) - static_cast<int>((m >> sh) & 15u);
+}
+// Signed counts of this lane's 4 code positions 4*(lane&3) .. +3 in one word:
+// shift the SWAR counters once, then extract fields with constant shifts.
+__device__ __forceinline__ void lane_counts(const Counts& c, int lane, int (&out)[4]) {
+    const int sh = 8 * (lane & 3);
+    const uint32_t pe = c.pe >> sh, me = c.me >> sh, po = c.po >> sh, mo = c.mo >> sh;
+    out[0] = static_cast<int>(pe & 15u) - static_cast<int>(me & 15u);
+    out[1] = static_cast<int>(po & 15u) - static_cast<int>(mo & 15u);
+    out[2] = static_cast<int>((pe >> 4) & 15u) - static_cast<int>((me >> 4) & 15u);
+    out[3] = static_cast<int>((po >> 4) & 15u) - static_cast<int>((mo >> 4) & 15u);
 }
 __device__ __forceinline__ double decode1(uint32_t code, double alpha) {
     return code == 1u ? alpha : (code == 2u ? -alpha : 0.0);
@@ -422,6 +433,7 @@ __global__ void __launch_bounds__(256) k_apply_quant(ApplyQArgs a, KeyTab kt, De
     warp_range(kt.ntiles, tb, te);
     const int lane = threadIdx.x & 31;
     double gsq = 0.0;
+    int isq = 0;  // sum of cnt^2 on the table path: gsq += isq * (alpha/N)^2
     uint64_t bad_idx = NO_ERR;
     const bool do_loc = a.loc != nullptr;
     if (tb < te && !skip) {
@@ -461,15 +473,13 @@ __global__ void __launch_bounds__(256) k_apply_quant(ApplyQArgs a, KeyTab kt, De
                     float g4[4];
                     if (do_loc) { g4[0] = gt[c].x; g4[1] = gt[c].y; g4[2] = gt[c].z; g4[3] = gt[c].w; }
                     float l4[4];
+                    int cq[4];
+                    lane_counts(cnt, lane, cq);
 #pragma unroll
                     for (int q = 0; q < 4; ++q) {
-                        const int ci = count_at(cnt, jb + q) + nr;
-                        w4[q] = __fsub_rn(w4[q], s_upd[ci]);
+                        w4[q] = __fsub_rn(w4[q], s_upd[cq[q] + nr]);
                         if (do_loc) l4[q] = __fmaf_rn(-a.eta_l, g4[q], w4[q]);
-                        if (a.gnorm != nullptr) {
-                            const double mv = s_mean[ci];
-                            gsq = __fma_rn(mv, mv, gsq);
-                        }
+                        isq += cq[q] * cq[q];
                     }
                     if (((cnt.rsv >> (2 * jb)) & 0xffu) != 0u) {
                         const int q = __ffs((cnt.rsv >> (2 * jb)) & 0x55u) / 2;
@@ -518,6 +528,7 @@ __global__ void __launch_bounds__(256) k_apply_quant(ApplyQArgs a, KeyTab kt, De
         }
     }
     if (a.gnorm != nullptr) {
+        gsq += static_cast<double>(isq) * tab.sq_scale;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) gsq += __shfl_xor_sync(FULL, gsq, o);
         if (lane == 0 && gsq != 0.0) atomicAdd(a.gnorm, gsq);

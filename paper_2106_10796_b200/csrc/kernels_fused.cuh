@@ -95,16 +95,12 @@ template <int NR, int APPLY, int WARPS, int S>
 __global__ void __launch_bounds__(WARPS * 32, 1) k_fused(FusedArgs a, KeyTab kt, DecodeTab tab) {
     using SM = FusedSmem<NR, APPLY, WARPS, S>;
     extern __shared__ __align__(128) unsigned char smem[];
-    __shared__ double s_mean[2 * MAX_RANKS + 1];
     __shared__ float s_upd[2 * MAX_RANKS + 1];
     p2p_wait2(a.xq, a.xa);
     const uint64_t e0v = a.err != nullptr ? *reinterpret_cast<volatile uint64_t*>(a.err) : ~0ull;
     const bool q_off = e0v != NO_ERR;        // sticky abort of quantization
     const bool a_off = e0v < a.skip_below;   // an error in round <= t-1: do not apply it
-    if (APPLY == APPLY_Q && threadIdx.x < 2 * NR + 1) {
-        s_mean[threadIdx.x] = tab.mean[threadIdx.x];
-        s_upd[threadIdx.x] = tab.upd[threadIdx.x];
-    }
+    if (APPLY == APPLY_Q && threadIdx.x < 2 * NR + 1) s_upd[threadIdx.x] = tab.upd[threadIdx.x];
     __syncthreads();
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -118,6 +114,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1) k_fused(FusedArgs a, KeyTab kt,
     warp_range(kt.ntiles, tb, te);
     uint64_t bad_idx = NO_ERR, bad_sym = NO_ERR;
     double gsq = 0.0;
+    int isq = 0;  // sum of cnt^2 (APPLY_Q): gsq += isq * (alpha/N)^2
     if (tb < te) {
         if (lane == 0) {
             for (int s = 0; s < S; ++s) tma::mbar_init(&bars[s], 1);
@@ -223,15 +220,13 @@ __global__ void __launch_bounds__(WARPS * 32, 1) k_fused(FusedArgs a, KeyTab kt,
 #pragma unroll
                             for (int r = 0; r < NR; ++r)
                                 count_add(cnt, *reinterpret_cast<const uint32_t*>(sx + r * CODE_WIN + off[r] + 4 * widx));
+                            int cq[4];
+                            lane_counts(cnt, lane, cq);
 #pragma unroll
                             for (int q = 0; q < 4; ++q) {
-                                const int ci = count_at(cnt, jb + q) + NR;
-                                wv[q] = __fsub_rn(wv[q], s_upd[ci]);
+                                wv[q] = __fsub_rn(wv[q], s_upd[cq[q] + NR]);
                                 l4[q] = __fmaf_rn(-a.eta_l, gv[q], wv[q]);
-                                if (a.gnorm != nullptr) {
-                                    const double mv = s_mean[ci];
-                                    gsq = __fma_rn(mv, mv, gsq);
-                                }
+                                isq += cq[q] * cq[q];
                             }
                             if (((cnt.rsv >> (2 * jb)) & 0xffu) != 0u) {
                                 const int q = __ffs((cnt.rsv >> (2 * jb)) & 0x55u) / 2;
@@ -305,7 +300,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1) k_fused(FusedArgs a, KeyTab kt,
                             float wn;
                             if constexpr (APPLY == APPLY_Q) {
                                 wn = __fsub_rn(a.W[e], s_upd[cn + NR]);
-                                if (a.gnorm != nullptr) gsq = __fma_rn(s_mean[cn + NR], s_mean[cn + NR], gsq);
+                                isq += cn * cn;
                                 if (rsv) bad_sym = static_cast<uint64_t>(e) < bad_sym ? static_cast<uint64_t>(e) : bad_sym;
                             } else {
                                 const float sv = a.gsum[e];
@@ -345,6 +340,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1) k_fused(FusedArgs a, KeyTab kt,
         }
     }
     if (a.gnorm != nullptr) {
+        gsq += static_cast<double>(isq) * tab.sq_scale;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) gsq += __shfl_xor_sync(FULL, gsq, o);
         if (lane == 0 && gsq != 0.0) atomicAdd(a.gnorm, gsq);
@@ -360,4 +356,215 @@ __global__ void __launch_bounds__(WARPS * 32, 1) k_fused(FusedArgs a, KeyTab kt,
     p2p_publish2(a.xq, a.xa, a.xq.counter != nullptr ? a.xq.counter : a.xa.counter);
 }
 
+}  // namespace cdsgd
+
+namespace cdsgd {
+// LDG variant of k_fused: same arithmetic and protocol, data moved with 128/256-bit
+// coalesced loads straight into registers (all loads of a tile issued first), two
+// 256-thread CTAs per SM instead of the TMA ring.
+template <int NR, int APPLY>
+__global__ void __launch_bounds__(256, 2) k_fused_ldg(FusedArgs a, KeyTab kt, DecodeTab tab) {
+    __shared__ float s_upd[2 * MAX_RANKS + 1];
+    p2p_wait2(a.xq, a.xa);
+    const uint64_t e0v = a.err != nullptr ? *reinterpret_cast<volatile uint64_t*>(a.err) : ~0ull;
+    const bool q_off = e0v != NO_ERR;
+    const bool a_off = e0v < a.skip_below;
+    if (APPLY == APPLY_Q && threadIdx.x < 2 * NR + 1) s_upd[threadIdx.x] = tab.upd[threadIdx.x];
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const uint32_t ahi = static_cast<uint32_t>(__double2hiint(a.alpha));
+    const uint32_t alo = static_cast<uint32_t>(__double2loint(a.alpha));
+    int64_t tb, te;
+    warp_range(kt.ntiles, tb, te);
+    uint64_t bad_idx = NO_ERR, bad_sym = NO_ERR;
+    double gsq = 0.0;
+    int isq = 0;
+    if (tb < te) {
+        TileCursor cc;
+        cc.seek(kt, tb);
+        for (int64_t ti = tb; ti < te; ++ti) {
+            cc.advance_to(kt, ti);
+            const int64_t j = ti - cc.t0;
+            const int64_t e0 = cc.e0 + j * TILE_ELEMS;
+            const int64_t w0 = cc.w0 + j * TILE_WORDS;
+            const int64_t ne64 = cc.e1 - e0;
+            const int ne = ne64 < TILE_ELEMS ? static_cast<int>(ne64) : TILE_ELEMS;
+            const int64_t nw64 = cc.w1 - w0;
+            const int nw = nw64 < TILE_WORDS ? static_cast<int>(nw64) : TILE_WORDS;
+            const bool fast = ne == TILE_ELEMS && aligned_to(a.g + e0, 16) && aligned_to(a.r_in + e0, 32) &&
+                              aligned_to(a.r_out + e0, 32) && aligned_to(a.W + e0, 16) && aligned_to(a.loc + e0, 16) &&
+                              (APPLY == APPLY_Q || aligned_to(a.gsum + e0, 16));
+            uint32_t myword = 0;
+            if (fast) {
+                float4 gv[CHUNKS], wv[CHUNKS], sv[CHUNKS];
+                d4 rv[CHUNKS];
+                uint32_t cw[APPLY == APPLY_Q ? NR : 1];
+                if constexpr (APPLY == APPLY_Q) {
+#pragma unroll
+                    for (int r = 0; r < NR; ++r) cw[r] = ld_word(a.gathered + r * a.stride + w0 + lane);
+                }
+#pragma unroll
+                for (int c = 0; c < CHUNKS; ++c) {
+                    const int64_t e = e0 + 128 * c + 4 * lane;
+                    gv[c] = ld_stream(a.g + e);
+                    rv[c] = ld_stream(a.r_in + e);
+                    wv[c] = ld_stream(a.W + e);
+                    if constexpr (APPLY == APPLY_F) sv[c] = ld_stream(a.gsum + e);
+                }
+                uint32_t v[CHUNKS];
+                bool bad = false;
+#pragma unroll
+                for (int c = 0; c < CHUNKS; ++c) {
+                    const int64_t e = e0 + 128 * c + 4 * lane;
+                    float g4[4] = {gv[c].x, gv[c].y, gv[c].z, gv[c].w};
+                    float w4[4] = {wv[c].x, wv[c].y, wv[c].z, wv[c].w};
+                    double r4[4] = {rv[c].x, rv[c].y, rv[c].z, rv[c].w};
+                    if (!a_off) {
+                        float l4[4];
+                        if constexpr (APPLY == APPLY_Q) {
+                            Counts cnt{0u, 0u, 0u, 0u, 0u};
+#pragma unroll
+                            for (int r = 0; r < NR; ++r) count_add(cnt, __shfl_sync(FULL, cw[r], 8 * c + (lane >> 2)));
+                            int cq[4];
+                            lane_counts(cnt, lane, cq);
+#pragma unroll
+                            for (int q = 0; q < 4; ++q) {
+                                w4[q] = __fsub_rn(w4[q], s_upd[cq[q] + NR]);
+                                l4[q] = __fmaf_rn(-a.eta_l, g4[q], w4[q]);
+                                isq += cq[q] * cq[q];
+                            }
+                            const int jb = 4 * (lane & 3);
+                            if (((cnt.rsv >> (2 * jb)) & 0xffu) != 0u) {
+                                const int q = __ffs((cnt.rsv >> (2 * jb)) & 0x55u) / 2;
+                                bad_sym = static_cast<uint64_t>(e + q) < bad_sym ? static_cast<uint64_t>(e + q) : bad_sym;
+                            }
+                        } else {
+                            const float s4[4] = {sv[c].x, sv[c].y, sv[c].z, sv[c].w};
+#pragma unroll
+                            for (int q = 0; q < 4; ++q) {
+                                w4[q] = __fmaf_rn(-a.scale, s4[q], w4[q]);
+                                l4[q] = __fmaf_rn(-a.eta_l, g4[q], w4[q]);
+                                if (a.gnorm != nullptr) {
+                                    const double m = s4[q] * a.inv_n;
+                                    gsq = __fma_rn(m, m, gsq);
+                                }
+                            }
+                        }
+                        st_stream(a.W + e, w4[0], w4[1], w4[2], w4[3]);
+                        st_stream(a.loc + e, l4[0], l4[1], l4[2], l4[3]);
+                    }
+                    if (!q_off) {
+                        double o[4];
+                        uint32_t code = 0;
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) code |= quant1_lean(r4[q], g4[q], a.alpha, ahi, alo, o[q], bad) << (2 * q);
+                        st_stream(a.r_out + e, o[0], o[1], o[2], o[3]);
+                        v[c] = code << (8 * (lane & 3));
+                    } else {
+                        v[c] = 0;
+                    }
+                }
+                if (__any_sync(FULL, bad)) {
+#pragma unroll
+                    for (int c = 0; c < CHUNKS; ++c) {
+                        const float g4[4] = {gv[c].x, gv[c].y, gv[c].z, gv[c].w};
+                        const double r4[4] = {rv[c].x, rv[c].y, rv[c].z, rv[c].w};
+#pragma unroll
+                        for (int q = 0; q < 4; ++q)
+                            if (nonfinite(__dadd_rn(r4[q], static_cast<double>(g4[q])))) {
+                                const uint64_t idx = a.tag | static_cast<uint64_t>(e0 + 128 * c + 4 * lane + q);
+                                bad_idx = idx < bad_idx ? idx : bad_idx;
+                            }
+                    }
+                }
+#pragma unroll
+                for (int c = 0; c < CHUNKS; ++c) v[c] |= __shfl_xor_sync(FULL, v[c], 1);
+#pragma unroll
+                for (int c = 0; c < CHUNKS; ++c) v[c] |= __shfl_xor_sync(FULL, v[c], 2);
+#pragma unroll
+                for (int c = 0; c < CHUNKS; ++c) {
+                    const uint32_t w = __shfl_sync(FULL, v[c], 4 * (lane & 7));
+                    if ((lane >> 3) == c) myword = w;
+                }
+            } else {
+                uint32_t cw[APPLY == APPLY_Q ? NR : 1];
+                if constexpr (APPLY == APPLY_Q) {
+#pragma unroll
+                    for (int r = 0; r < NR; ++r) cw[r] = lane < nw ? a.gathered[r * a.stride + w0 + lane] : 0u;
+                }
+#pragma unroll 2
+                for (int s = 0; s < TILE_ELEMS / 32; ++s) {
+                    const int el = 32 * s + lane;
+                    int cn = 0;
+                    bool rsv = false;
+                    if constexpr (APPLY == APPLY_Q) {
+#pragma unroll
+                        for (int r = 0; r < NR; ++r) {
+                            const uint32_t cd = (__shfl_sync(FULL, cw[r], 2 * s + (lane >> 4)) >> (2 * (lane & 15))) & 3u;
+                            rsv |= cd == 3u;
+                            cn += (cd == 1u) - (cd == 2u);
+                        }
+                    }
+                    bool p = false, m = false;
+                    if (el < ne) {
+                        const int64_t e = e0 + el;
+                        const float gval = a.g[e];
+                        if (!a_off) {
+                            float wn;
+                            if constexpr (APPLY == APPLY_Q) {
+                                wn = __fsub_rn(a.W[e], s_upd[cn + NR]);
+                                isq += cn * cn;
+                                if (rsv) bad_sym = static_cast<uint64_t>(e) < bad_sym ? static_cast<uint64_t>(e) : bad_sym;
+                            } else {
+                                const float sv1 = a.gsum[e];
+                                wn = __fmaf_rn(-a.scale, sv1, a.W[e]);
+                                if (a.gnorm != nullptr) { const double mm = sv1 * a.inv_n; gsq = __fma_rn(mm, mm, gsq); }
+                            }
+                            a.W[e] = wn;
+                            a.loc[e] = __fmaf_rn(-a.eta_l, gval, wn);
+                        }
+                        if (!q_off) {
+                            double o;
+                            bool b;
+                            const uint32_t code = quant1(a.r_in[e], gval, a.alpha, o, b);
+                            a.r_out[e] = o;
+                            p = code == 1u;
+                            m = code == 2u;
+                            if (b) {
+                                const uint64_t idx = a.tag | static_cast<uint64_t>(e);
+                                bad_idx = idx < bad_idx ? idx : bad_idx;
+                            }
+                        }
+                    }
+                    const uint32_t pm = __ballot_sync(FULL, p);
+                    const uint32_t mm = __ballot_sync(FULL, m);
+                    if (lane == 2 * s) myword = interleave_codes(pm, mm);
+                    if (lane == 2 * s + 1) myword = interleave_codes(pm >> 16, mm >> 16);
+                }
+            }
+            if (lane < nw && !q_off) {
+                if (a.xq.nranks > 0) {
+                    for (int r = 0; r < a.xq.nranks; ++r) a.xq.dst[r][w0 + lane] = myword;
+                } else {
+                    a.words[w0 + lane] = myword;
+                }
+            }
+        }
+    }
+    if (a.gnorm != nullptr) {
+        gsq += static_cast<double>(isq) * tab.sq_scale;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) gsq += __shfl_xor_sync(FULL, gsq, o);
+        if (lane == 0 && gsq != 0.0) atomicAdd(a.gnorm, gsq);
+    }
+    if (a.err != nullptr) {
+        bad_idx = warp_min_u64(bad_idx);
+        bad_sym = warp_min_u64(bad_sym);
+        if (lane == 0 && bad_idx != NO_ERR)
+            atomicMin(reinterpret_cast<unsigned long long*>(a.err), static_cast<unsigned long long>(bad_idx));
+        if (lane == 0 && bad_sym != NO_ERR)
+            atomicMin(reinterpret_cast<unsigned long long*>(a.err + 1), static_cast<unsigned long long>(bad_sym));
+    }
+    p2p_publish2(a.xq, a.xa, a.xq.counter != nullptr ? a.xq.counter : a.xa.counter);
+}
 }  // namespace cdsgd

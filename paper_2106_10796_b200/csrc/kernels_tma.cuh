@@ -367,13 +367,14 @@ __global__ void __launch_bounds__(WARPS * 32, 1) k_apply_quant_tma(ApplyQArgs a,
 #pragma unroll
                     for (int r = 0; r < NR; ++r) count_add(cnt, cw[c][r]);
                     float l4[4];
+                    int cq[4];
+                    lane_counts(cnt, lane, cq);
 #pragma unroll
                     for (int q = 0; q < 4; ++q) {
-                        const int ci = count_at(cnt, jb + q) + NR;
-                        w4[c][q] = __fsub_rn(w4[c][q], s_upd[ci]);
+                        w4[c][q] = __fsub_rn(w4[c][q], s_upd[cq[q] + NR]);
                         if (do_loc) l4[q] = __fmaf_rn(-a.eta_l, g4[c][q], w4[c][q]);
                         if (a.gnorm != nullptr) {
-                            const double mv = s_mean[ci];
+                            const double mv = s_mean[cq[q] + NR];
                             gsq = __fma_rn(mv, mv, gsq);
                         }
                     }
