@@ -46,8 +46,10 @@ def parse():
     ap.add_argument("--workload", default="resnet50", help="resnet50 | resnet20 | vgg16 | single:<n> | keys:a,b,..")
     ap.add_argument("--k", type=int, default=4)
     ap.add_argument("--alpha", type=float, default=0.5)
-    ap.add_argument("--exchange", choices=("p2p", "nccl"), default="p2p",
-                    help="p2p: all-gather fused into K1 over NVLink (symmetric memory); nccl: ncclAllGather")
+    ap.add_argument("--exchange", choices=("p2p", "p2p-exact", "nccl"), default="p2p",
+                    help="p2p: code all-gather fused into K1 over NVLink (symmetric memory), correction by "
+                         "ncclAllReduce; p2p-exact: corrections by the exact sharded NVLink reduce too; "
+                         "nccl: ncclAllGather + ncclAllReduce")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="budget of the cpu_baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -284,6 +286,9 @@ def run_ours(args):
         "local_update": 3 * 4 * n,
         # apply(t-1) + quantize(t): g 4 | r 8+8 | W 4+4 | loc 4 | codes in N/4 + out 1/4
         "fused": 4 * n + 16 * n + 8 * n + 4 * n + world * 4 * nw + 4 * nw,
+        # P2P correction: stage g (4+4); reduce of my shard n/N: N stage reads + W r/w (+ N-1 remote W writes)
+        "stage": 8 * n,
+        "reduce": (world * 4 * n + 4 * n + world * 4 * n) // max(world, 1),
     }
     kernels = {}
     for kname, nbytes in alg.items():
@@ -295,6 +300,8 @@ def run_ours(args):
                               "bytes_per_elem": round(nbytes / n, 4), "achieved_gbs": gbs, "frac": gbs / peak,
                               "share_of_step": st["ms"] / (ms if world == 1 else ev0.elapsed_time(ev1))}
     dom = max(kernels, key=lambda k: prof[k]["ms"])
+    waits = {k: {"launches": prof[k]["n"], "avg_us": 1e3 * prof[k]["ms"] / prof[k]["n"]}
+             for k in ("wait",) if prof[k]["n"]}
     roof = {"bound": "hbm", "kernel": dom, "achieved": kernels[dom]["achieved_gbs"], "peak": peak, "unit": "GB/s",
             "frac": kernels[dom]["achieved_gbs"] / peak, "traffic": ncu_traffic(args.workload, dom),
             "algorithmic_bytes_per_launch": alg[dom], "peak_source": peak_src}
@@ -366,11 +373,13 @@ def run_ours(args):
                        "n_per_rank": n, "keys": len(layout), "k": args.k, "alpha": args.alpha, "algo": "cdsgd",
                        "warmup_n": 0, "residual": "fp64 (bit-exact)", "weights": "fp32",
                        "exchange": ("codes all-gathered inside K1 by NVLink stores to peer memory (symmetric "
-                                    "memory, release/acquire flags)" if args.exchange == "p2p" and world > 1 else
-                                    "ncclAllGather(packed codes)") + "; ncclAllReduce(fp32) every k-th round",
+                                    "memory, release/acquire flags)" if args.exchange != "nccl" and world > 1 else
+                                    "ncclAllGather(packed codes)") + (
+                                    "; exact sharded fp64 NVLink reduce every k-th round" if
+                                    args.exchange == "p2p-exact" else "; ncclAllReduce(fp32) every k-th round"),
                        "l2": f"inputs larger than L2: {(20 * n) / 2**20:.0f} MiB touched per step per rank",
                        "parallelism": f"dp{world}"},
-            "roofline": roof, "kernels": kernels, "exchange": exch, "cpu_baseline": cpu, "e2e": e2e,
+            "roofline": roof, "kernels": kernels, "waits": waits, "exchange": exch, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches, "clocks": clk,
         }
         print(json.dumps(line), flush=True)

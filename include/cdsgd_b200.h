@@ -208,19 +208,27 @@ int cdsgd_engine_round_compressed(const cdsgd_engine* eng, int64_t t);
  * stores each packed word directly into every rank's slot and publishes a release
  * flag; K2 acquires all ranks' flags (spin on local memory, ~10 s timeout ->
  * CDSGD_ERR_STATE at cdsgd_engine_check) and releases the slot. Correction rounds
- * keep ncclAllReduce. Requires nranks <= 8 (one NVSwitch box). */
-int64_t cdsgd_p2p_bytes(int32_t nranks, int64_t words);
-int cdsgd_engine_attach_p2p(cdsgd_engine* eng, void* const* peer_bases, int32_t nranks);
+ * use ncclAllReduce on the engine's stream (overlapped with compute) unless
+ * exact_correction != 0: then g_t is staged in the symmetric buffer and in the next
+ * round every rank reduces its shard of elements from all ranks' stages (fp64,
+ * ascending rank — bitwise the reference's sum, engine.py:250-255), applies
+ * W -= eta*mean and stores the W' shard into every rank's replica (no NCCL at all).
+ * Requires nranks <= 8 (one NVSwitch box). */
+int64_t cdsgd_p2p_bytes(int32_t nranks, int64_t n, int64_t words);
+/* Byte offset of the W replica inside the symmetric buffer (attach moves W there:
+ * peers store their W' shards of correction rounds into it). */
+int64_t cdsgd_p2p_weights_offset(int32_t nranks, int64_t n, int64_t words);
+int cdsgd_engine_attach_p2p(cdsgd_engine* eng, void* const* peer_bases, int32_t nranks, int32_t exact_correction);
 /* Make `stream` wait for every exchange the engine has issued so far. */
 int cdsgd_engine_join(cdsgd_engine* eng, void* stream);
 /* Per-kernel timing with CUDA events recorded on the launching streams around
  * each K1 / K2 / K3 / local-update launch and each NCCL call, between _begin and
- * _end. _end synchronises and writes 12 doubles:
- * {quant_ms, quant_n, apply_quant_ms, apply_quant_n, apply_full_ms, apply_full_n,
- *  local_ms, local_n, exchange_ms, exchange_n, fused_ms, fused_n} (ms are sums over
- * launches; "fused" = apply(t-1) + quantize(t) in one kernel). */
+ * _end. _end synchronises and writes 18 doubles, (ms, launches) per class:
+ * quantize, apply_quant, apply_full, local_update, exchange (NCCL), fused
+ * (apply(t-1) + quantize(t) in one kernel), stage, reduce (P2P correction), wait
+ * (P2P correction completion). */
 int cdsgd_engine_profile_begin(cdsgd_engine* eng);
-int cdsgd_engine_profile_end(cdsgd_engine* eng, double* out12);
+int cdsgd_engine_profile_end(cdsgd_engine* eng, double* out18);
 
 #ifdef __cplusplus
 }

@@ -78,8 +78,9 @@ _SIGS = {
     "cdsgd_engine_check": (C.c_int, [vp, vp, C.POINTER(i64), C.POINTER(i64)]),
     "cdsgd_engine_round_compressed": (C.c_int, [vp, i64]),
     "cdsgd_engine_join": (C.c_int, [vp, vp]),
-    "cdsgd_p2p_bytes": (i64, [i32, i64]),
-    "cdsgd_engine_attach_p2p": (C.c_int, [vp, C.POINTER(vp), i32]),
+    "cdsgd_p2p_bytes": (i64, [i32, i64, i64]),
+    "cdsgd_p2p_weights_offset": (i64, [i32, i64, i64]),
+    "cdsgd_engine_attach_p2p": (C.c_int, [vp, C.POINTER(vp), i32, i32]),
     "cdsgd_engine_profile_begin": (C.c_int, [vp]),
     "cdsgd_engine_profile_end": (C.c_int, [vp, C.POINTER(f64)]),
 }

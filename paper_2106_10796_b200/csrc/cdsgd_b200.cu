@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <nccl.h>
 
+#include <algorithm>
 #include <atomic>
 #include <cmath>
 #include <cstdarg>
@@ -16,6 +17,7 @@
 #include "kernels.cuh"
 #include "kernels_tma.cuh"
 #include "kernels_fused.cuh"
+#include "kernels_corr.cuh"
 
 using namespace cdsgd;
 
@@ -420,7 +422,8 @@ inline bool pow2(int n) { return n > 0 && (n & (n - 1)) == 0; }
 int launch_apply_quant(const cdsgd_layout* L, float* W, const uint32_t* gathered, int nr, int64_t stride,
                        double alpha, double eta_g, const float* gnext, float* loc, double eta_l, uint64_t* err,
                        uint64_t skip_below, double* gnorm, const DecodeTab* tab_in, int exact_in,
-                       cudaStream_t st, const P2PArgs* x = nullptr) {
+                       cudaStream_t st, const P2PArgs* x = nullptr, float* gstage = nullptr,
+                       const P2PArgs* xs = nullptr) {
     if (L == nullptr) return fail(CDSGD_ERR_ARG, "layout is NULL");
     if (nr < 1 || nr > MAX_RANKS - 1) return fail(CDSGD_ERR_ARG, "nranks must be in [1, %d]", MAX_RANKS - 1);
     if ((gnext == nullptr) != (loc == nullptr)) return fail(CDSGD_ERR_ARG, "g_next and loc_out go together");
@@ -441,6 +444,8 @@ int launch_apply_quant(const cdsgd_layout* L, float* W, const uint32_t* gathered
     a.skip_below = skip_below;
     a.gnorm = gnorm;
     a.x = x != nullptr ? *x : P2PArgs{};
+    a.gstage = gstage;
+    a.xs = xs != nullptr ? *xs : P2PArgs{};
     DecodeTab tab;
     int exact;
     if (tab_in != nullptr) {
@@ -456,7 +461,7 @@ int launch_apply_quant(const cdsgd_layout* L, float* W, const uint32_t* gathered
         const char* e = getenv("CDSGD_K2_TMA");
         return e != nullptr && e[0] == '1';
     }();
-    if (k2_tma && exact && nr <= 8 && a.x.nranks == 0) {
+    if (k2_tma && exact && nr <= 8 && a.x.nranks == 0 && gstage == nullptr) {
         int rc = CDSGD_OK;
 #define AQT(R)                                               \
     case R: rc = launch_aq_tma_cfg<R>(a, kt, tab, st); break;
@@ -540,10 +545,12 @@ int launch_fused_cfg(const FusedArgs& a, const KeyTab& kt, const DecodeTab& tab,
         default: return launch_fused_t<NR, AP, 12, 2>(a, kt, tab, st);
     }
 }
-int launch_fused(int nr, bool apply_quant, const FusedArgs& a, const KeyTab& kt, const DecodeTab& tab,
-                 cudaStream_t st) {
+int launch_fused(int nr, int apply, const FusedArgs& a, const KeyTab& kt, const DecodeTab& tab, cudaStream_t st) {
     int rc;
-    if (!apply_quant) {
+    if (apply == APPLY_L) {  // W is final (P2P correction): only loc = W - eta_l*g and quantize
+        k_fused_ldg<1, APPLY_L><<<tile_grid(k_fused_ldg<1, APPLY_L>, kt.ntiles), THREADS, 0, st>>>(a, kt, tab);
+        rc = CDSGD_OK;
+    } else if (apply == APPLY_F) {
         rc = launch_fused_cfg<1, APPLY_F>(a, kt, tab, st);
     } else {
         switch (nr) {
@@ -659,9 +666,18 @@ struct cdsgd_engine {
     int64_t off_slot[2] = {0, 0}, off_ready = 0, off_freed = 0;
     int64_t last_use[2] = {-1, -1};  // last compressed round that filled slot p
     bool xused[2] = {false, false};  // round parity p used the NCCL stream
-    unsigned int* counters = nullptr;  // [2] grid-completion counters (K1/fused, K2)
+    unsigned int* counters = nullptr;  // [4] grid-completion counters (K1/fused, K2, stage, reduce)
+    // P2P correction rounds (sharded exact reduce over NVLink, no NCCL)
+    int64_t off_W = 0, off_stage[2] = {0, 0}, off_gready = 0, off_gfreed = 0, off_wdone = 0, off_gpart = 0;
+    int64_t last_stage[2] = {-1, -1};  // last correction round that used staging slot s
+    int64_t ncorr = 0;                 // P2P correction rounds staged so far (slot = ncorr & 1)
+    int pend_slot = 0;                 // staging slot of the pending correction round
+    int64_t s0 = 0, s1 = 0;            // this rank's shard of elements
+    double* gacc = nullptr;            // shard sum(mean^2) accumulator
     bool fuse = false;                 // apply(t-1) + quantize(t) in one kernel (N=1 or P2P)
-    // profiling: event pairs per kernel class (0 quant, 1 apply_q, 2 apply_f, 3 local, 4 exchange, 5 fused)
+    bool pcorr = false;                // P2P mode: correction rounds by the exact sharded NVLink reduce
+    // profiling: event pairs per kernel class (0 quant, 1 apply_q, 2 apply_f, 3 local, 4 exchange, 5 fused,
+    // 6 stage, 7 reduce, 8 wait)
     bool prof = false;
     std::vector<cudaEvent_t> ev_pool;
     size_t ev_used = 0;
@@ -705,10 +721,117 @@ int round_compressed(const cdsgd_engine* E, int64_t t, bool* out) {
 
 int64_t words_of(const cdsgd_engine* E) { return E->L->nwords; }
 
+// ---- P2P correction rounds (kernels_corr.cuh)
+template <typename T>
+T* at(char* base, int64_t off) { return reinterpret_cast<T*>(base + off); }
+
+// Round t is a correction: g_t goes to staging slot ncorr & 1 where every rank can
+// read it. prepare_stage fills the destination + protocol and advances the state;
+// the copy is then either fused into K2 (which reads g_t anyway) or run by k_stage.
+void prepare_stage(cdsgd_engine* E, int64_t t, float** dst, P2PArgs* x) {
+    const int nr = E->d.nranks, me = E->d.rank;
+    const int s = static_cast<int>(E->ncorr & 1);
+    char* local = E->peer[me];
+    *dst = at<float>(local, E->off_stage[s]);
+    *x = P2PArgs{};
+    x->nranks = nr;
+    for (int r = 0; r < nr; ++r) x->publish[r] = at<uint64_t>(E->peer[r], E->off_gready) + s * nr + me;
+    x->wait_flags = at<const uint64_t>(local, E->off_gfreed) + s * nr;
+    x->wait_value = E->last_stage[s] >= 0 ? static_cast<uint64_t>(E->last_stage[s]) + 1 : 0;
+    x->publish_value = static_cast<uint64_t>(t) + 1;
+    x->counter = E->counters + 2;
+    x->err = E->d.err;
+    E->last_stage[s] = t;
+    E->pend_slot = s;
+    E->ncorr += 1;
+}
+
+int p2p_stage(cdsgd_engine* E, int64_t t, const float* g, cudaStream_t C) {
+    StageArgs a{};
+    a.g = g;
+    a.n = E->L->n;
+    prepare_stage(E, t, &a.stage, &a.x);
+    const long pi = prof_start(E, 6, C);
+    k_stage<<<flat_grid(k_stage, (a.n + 3) / 4), THREADS, 0, C>>>(a);
+    prof_stop(E, pi, C);
+    LAUNCH_CHECK();
+    return CDSGD_OK;
+}
+
+template <int NR>
+void launch_reduce_t(const ReduceArgs& a, int64_t len, cudaStream_t C) {
+    k_reduce<NR><<<flat_grid(k_reduce<NR>, (len + 3) / 4), THREADS, 0, C>>>(a);
+}
+
+// Apply correction round p: reduce my shard from every rank's stage, broadcast W',
+// then wait until every shard has landed (W == W_{p+1} everywhere).
+int p2p_reduce(cdsgd_engine* E, int64_t p, cudaStream_t C) {
+    const int nr = E->d.nranks, me = E->d.rank;
+    const int s = E->pend_slot;
+    char* local = E->peer[me];
+    ReduceArgs a{};
+    for (int r = 0; r < nr; ++r) {
+        a.stage[r] = at<const float>(E->peer[r], E->off_stage[s]);
+        a.Wdst[r] = at<float>(E->peer[r], E->off_W);
+        a.gpart_dst[r] = at<double>(E->peer[r], E->off_gpart) + s * nr + me;
+        a.xa.publish[r] = at<uint64_t>(E->peer[r], E->off_gfreed) + s * nr + me;
+        a.xb.publish[r] = at<uint64_t>(E->peer[r], E->off_wdone) + me;
+    }
+    a.W = at<const float>(local, E->off_W);
+    a.s0 = E->s0;
+    a.s1 = E->s1;
+    a.nranks = nr;
+    a.eta_g = E->d.eta_global;
+    a.inv_n = pow2(nr) ? 1.0 / nr : 0.0;
+    a.gacc = E->gacc;
+    a.xa.nranks = nr;
+    a.xa.wait_flags = at<const uint64_t>(local, E->off_gready) + s * nr;
+    a.xa.wait_value = static_cast<uint64_t>(p) + 1;
+    a.xa.publish_value = static_cast<uint64_t>(p) + 1;
+    a.xa.counter = E->counters + 3;
+    a.xa.err = E->d.err;
+    a.xb.nranks = nr;
+    a.xb.publish_value = static_cast<uint64_t>(p) + 1;
+    CUDA_TRY(cudaMemsetAsync(E->gacc, 0, sizeof(double), C));
+    const long pi = prof_start(E, 7, C);
+    const int64_t len = E->s1 - E->s0;
+    switch (nr) {
+        case 2: launch_reduce_t<2>(a, len, C); break;
+        case 3: launch_reduce_t<3>(a, len, C); break;
+        case 4: launch_reduce_t<4>(a, len, C); break;
+        case 5: launch_reduce_t<5>(a, len, C); break;
+        case 6: launch_reduce_t<6>(a, len, C); break;
+        case 7: launch_reduce_t<7>(a, len, C); break;
+        case 8: launch_reduce_t<8>(a, len, C); break;
+        default: return fail(CDSGD_ERR_ARG, "P2P correction supports 2..8 ranks");
+    }
+    LAUNCH_CHECK();
+    P2PArgs w{};
+    w.nranks = nr;
+    w.wait_flags = at<const uint64_t>(local, E->off_wdone);
+    w.wait_value = static_cast<uint64_t>(p) + 1;
+    w.err = E->d.err;
+    double* gn = (E->d.gnorm_sq != nullptr && E->d.gnorm_ring > 0) ? E->d.gnorm_sq + (p % E->d.gnorm_ring) : nullptr;
+    prof_stop(E, pi, C);
+    const long pw = prof_start(E, 8, C);
+    k_wait_sum<<<1, 32, 0, C>>>(w, at<const double>(local, E->off_gpart) + s * nr, nr, gn);
+    prof_stop(E, pw, C);
+    LAUNCH_CHECK();
+    return CDSGD_OK;
+}
+
 // Finish round p: wait for its exchange, then K2 (codes) or K3 (full) fused with
 // the local update from g_next (nullable).
-int engine_apply(cdsgd_engine* E, int64_t p, bool comp, const float* gp, const float* gnext, cudaStream_t C) {
+int engine_apply(cdsgd_engine* E, int64_t p, bool comp, const float* gp, const float* gnext, cudaStream_t C,
+                 float* gstage = nullptr, const P2PArgs* xs = nullptr) {
     const int nr = E->d.nranks;
+    if (!comp && E->p2p && E->pcorr) {  // P2P correction: exact sharded reduce, then (optionally) the local update
+        int rc = p2p_reduce(E, p, C);
+        if (rc == CDSGD_OK && gnext != nullptr)
+            rc = cdsgd_local_update(E->d.weights, CDSGD_F32, gnext, CDSGD_F32, E->d.loc, CDSGD_F32, E->L->n,
+                                    E->d.eta_local, C);
+        return rc;
+    }
     if (nr > 1 && E->xused[p & 1]) CUDA_TRY(cudaStreamWaitEvent(C, E->evX[p & 1], 0));
     const int64_t rel = p - E->err_base + 1;
     const uint64_t skip_below = rel <= 0 ? 0ull : (static_cast<uint64_t>(rel) << CDSGD_INDEX_BITS);
@@ -735,7 +858,7 @@ int engine_apply(cdsgd_engine* E, int64_t p, bool comp, const float* gp, const f
         const long pi = prof_start(E, 1, C);
         const int rc = launch_apply_quant(E->L, E->d.weights, E->d.gathered[p & 1], nr, words_of(E), E->d.alpha,
                                           E->d.eta_global, gnext, loc, E->d.eta_local, E->d.err, skip_below, gn,
-                                          &E->tab, E->exact, C, &x);
+                                          &E->tab, E->exact, C, &x, gstage, xs);
         prof_stop(E, pi, C);
         return rc;
     }
@@ -798,22 +921,39 @@ extern "C" int cdsgd_engine_create(const cdsgd_engine_desc* d, const cdsgd_layou
 
 namespace {
 int64_t align256(int64_t v) { return (v + 255) & ~int64_t(255); }
-void p2p_offsets(int32_t nranks, int64_t words, int64_t* slot1, int64_t* ready, int64_t* freed, int64_t* total) {
-    const int64_t slot = align256(static_cast<int64_t>(nranks) * words * 4);
-    *slot1 = slot;
-    *ready = 2 * slot;
-    *freed = *ready + align256(2 * nranks * 8);
-    *total = *freed + align256(2 * nranks * 8);
+// Symmetric buffer: codes slot 0 | slot 1 | ready[2][N] | freed[2][N] | W [n] |
+// stage 0 [n] | stage 1 [n] | gready[2][N] | gfreed[2][N] | wdone[N] | gpart[2][N] | end
+void p2p_offsets(int32_t nranks, int64_t n, int64_t words, int64_t* off /* [12] */) {
+    const int64_t flags = align256(2 * nranks * 8);
+    off[0] = 0;
+    off[1] = align256(static_cast<int64_t>(nranks) * words * 4);
+    off[2] = 2 * off[1];
+    off[3] = off[2] + flags;
+    off[4] = off[3] + flags;
+    off[5] = off[4] + align256(4 * n);
+    off[6] = off[5] + align256(4 * n);
+    off[7] = off[6] + align256(4 * n);
+    off[8] = off[7] + flags;
+    off[9] = off[8] + flags;
+    off[10] = off[9] + align256(nranks * 8);
+    off[11] = off[10] + flags;
 }
 }  // namespace
 
-extern "C" int64_t cdsgd_p2p_bytes(int32_t nranks, int64_t words) {
-    int64_t a, b, c, total;
-    p2p_offsets(nranks, words, &a, &b, &c, &total);
-    return total;
+extern "C" int64_t cdsgd_p2p_bytes(int32_t nranks, int64_t n, int64_t words) {
+    int64_t off[12];
+    p2p_offsets(nranks, n, words, off);
+    return off[11];
 }
 
-extern "C" int cdsgd_engine_attach_p2p(cdsgd_engine* E, void* const* peer_bases, int32_t nranks) {
+extern "C" int64_t cdsgd_p2p_weights_offset(int32_t nranks, int64_t n, int64_t words) {
+    int64_t off[12];
+    p2p_offsets(nranks, n, words, off);
+    return off[4];
+}
+
+extern "C" int cdsgd_engine_attach_p2p(cdsgd_engine* E, void* const* peer_bases, int32_t nranks,
+                                       int32_t exact_correction) {
     if (E == nullptr || peer_bases == nullptr) return fail(CDSGD_ERR_ARG, "NULL argument");
     if (nranks != E->d.nranks || nranks < 2) return fail(CDSGD_ERR_ARG, "attach_p2p needs nranks == workers >= 2");
     if (nranks > MAX_RANKS_P2P) return fail(CDSGD_ERR_ARG, "fused exchange supports at most %d ranks", MAX_RANKS_P2P);
@@ -824,17 +964,38 @@ extern "C" int cdsgd_engine_attach_p2p(cdsgd_engine* E, void* const* peer_bases,
             return fail(CDSGD_ERR_ARG, "peer base %d is NULL or not 256-byte aligned", r);
         E->peer[r] = static_cast<char*>(peer_bases[r]);
     }
-    int64_t total;
-    p2p_offsets(nranks, E->L->nwords, &E->off_slot[1], &E->off_ready, &E->off_freed, &total);
-    E->off_slot[0] = 0;
+    int64_t off[12];
+    p2p_offsets(nranks, E->L->n, E->L->nwords, off);
+    E->off_slot[0] = off[0];
+    E->off_slot[1] = off[1];
+    E->off_ready = off[2];
+    E->off_freed = off[3];
+    E->off_W = off[4];
+    E->off_stage[0] = off[5];
+    E->off_stage[1] = off[6];
+    E->off_gready = off[7];
+    E->off_gfreed = off[8];
+    E->off_wdone = off[9];
+    E->off_gpart = off[10];
     char* local = E->peer[E->d.rank];
     E->d.gathered[0] = reinterpret_cast<uint32_t*>(local + E->off_slot[0]);
     E->d.gathered[1] = reinterpret_cast<uint32_t*>(local + E->off_slot[1]);
-    if (E->counters == nullptr) {
-        CUDA_TRY(cudaMalloc(&E->counters, 2 * sizeof(unsigned int)));
-        CUDA_TRY(cudaMemset(E->counters, 0, 2 * sizeof(unsigned int)));
+    // the W replica moves into symmetric memory (peers store their W' shards into it)
+    float* wsym = reinterpret_cast<float*>(local + E->off_W);
+    if (wsym != E->d.weights) {
+        CUDA_TRY(cudaMemcpy(wsym, E->d.weights, 4 * E->L->n, cudaMemcpyDeviceToDevice));
+        E->d.weights = wsym;
     }
+    const int64_t chunk = (((E->L->n + nranks - 1) / nranks) + 3) / 4 * 4;
+    E->s0 = std::min<int64_t>(E->L->n, chunk * E->d.rank);
+    E->s1 = std::min<int64_t>(E->L->n, E->s0 + chunk);
+    if (E->counters == nullptr) {
+        CUDA_TRY(cudaMalloc(&E->counters, 4 * sizeof(unsigned int)));
+        CUDA_TRY(cudaMemset(E->counters, 0, 4 * sizeof(unsigned int)));
+    }
+    if (E->gacc == nullptr) CUDA_TRY(cudaMalloc(&E->gacc, sizeof(double)));
     E->p2p = true;
+    E->pcorr = exact_correction != 0;
     {
         const char* nf = getenv("CDSGD_NO_FUSE");
         E->fuse = !(nf != nullptr && nf[0] == '1');
@@ -861,7 +1022,7 @@ extern "C" int cdsgd_engine_profile_begin(cdsgd_engine* E) {
 extern "C" int cdsgd_engine_profile_end(cdsgd_engine* E, double* out) {
     if (E == nullptr || out == nullptr) return fail(CDSGD_ERR_ARG, "NULL argument");
     E->prof = false;
-    for (int i = 0; i < 12; ++i) out[i] = 0.0;
+    for (int i = 0; i < 18; ++i) out[i] = 0.0;
     for (const auto& m : E->prof_marks) {
         CUDA_TRY(cudaEventSynchronize(E->ev_pool[m.second + 1]));
         float ms = 0.f;
@@ -884,6 +1045,7 @@ extern "C" int cdsgd_engine_destroy(cdsgd_engine* E) {
     }
     if (E->xs) cudaStreamDestroy(E->xs);
     if (E->counters) cudaFree(E->counters);
+    if (E->gacc) cudaFree(E->gacc);
     delete E;
     return CDSGD_OK;
 }
@@ -908,6 +1070,65 @@ extern "C" int cdsgd_engine_step(cdsgd_engine* E, const float* g, void* stream) 
     const int64_t nw = words_of(E);
     uint32_t* mine = E->d.gathered[t & 1] + static_cast<int64_t>(E->d.rank) * nw;
     const bool sync_path0 = !E->uses_local || t < E->n_warmup - 1;
+    if (E->p2p && E->pcorr && E->pending && !E->pend_comp) {
+        // ---- previous round was a P2P correction: W_t = reduce(stage_{t-1}) first
+        rc = p2p_reduce(E, E->pend_t, C);
+        if (rc != CDSGD_OK) return rc;
+        E->pending = false;
+        E->rlog.push_back(static_cast<int8_t>(E->rcur));
+        if (comp) {
+            // quantize(t) + loc_{t+1} = W_t - eta_l*g_t in one pass
+            const int p = static_cast<int>(t & 1);
+            char* local = E->peer[E->d.rank];
+            FusedArgs a{};
+            a.g = g;
+            a.r_in = E->d.residual[E->rcur];
+            a.r_out = E->d.residual[E->rcur ^ 1];
+            a.words = mine;
+            a.alpha = E->d.alpha;
+            a.tag = static_cast<uint64_t>(t - E->err_base) << CDSGD_INDEX_BITS;
+            a.W = E->d.weights;
+            a.loc = E->d.loc;
+            a.eta_l = static_cast<float>(E->d.eta_local);
+            a.skip_below = 0;
+            a.err = E->d.err;
+            a.xq.nranks = nr;
+            for (int r = 0; r < nr; ++r) {
+                a.xq.dst[r] = reinterpret_cast<uint32_t*>(E->peer[r] + E->off_slot[p]) + static_cast<int64_t>(E->d.rank) * nw;
+                a.xq.publish[r] = reinterpret_cast<uint64_t*>(E->peer[r] + E->off_ready) + p * nr + E->d.rank;
+            }
+            a.xq.wait_flags = reinterpret_cast<const uint64_t*>(local + E->off_freed) + p * nr;
+            a.xq.wait_value = E->last_use[p] >= 0 ? static_cast<uint64_t>(E->last_use[p]) + 1 : 0;
+            a.xq.publish_value = static_cast<uint64_t>(t) + 1;
+            a.xq.counter = E->counters;
+            a.xq.err = E->d.err;
+            E->last_use[p] = t;
+            const long pi = prof_start(E, 5, C);
+            rc = launch_fused(nr, APPLY_L, a, E->L->tab(), E->tab, C);
+            prof_stop(E, pi, C);
+            if (rc != CDSGD_OK) return rc;
+            E->rcur ^= 1;
+            E->pending = true;
+            E->pend_t = t;
+            E->pend_comp = true;
+            E->pend_grad = g;
+        } else {
+            // another correction round: loc_{t+1} = W_t - eta_l*g_t, then stage g_t
+            rc = cdsgd_local_update(E->d.weights, CDSGD_F32, g, CDSGD_F32, E->d.loc, CDSGD_F32, E->L->n,
+                                    E->d.eta_local, stream);
+            if (rc != CDSGD_OK) return rc;
+            rc = p2p_stage(E, t, g, C);
+            if (rc != CDSGD_OK) return rc;
+            E->pending = true;
+            E->pend_t = t;
+            E->pend_comp = false;
+            E->pend_grad = g;
+        }
+        E->xused[t & 1] = false;
+        E->compute_is_loc = true;
+        E->t = t + 1;
+        return CDSGD_OK;
+    }
     if (E->fuse && comp && E->pending && !sync_path0 && (E->pend_comp || nr == 1)) {
         // ---- one kernel: apply(t-1) fused with quantize(t); both read g_t once
         const int64_t pnd = E->pend_t;
@@ -956,7 +1177,7 @@ extern "C" int cdsgd_engine_step(cdsgd_engine* E, const float* g, void* stream) 
         }
         E->rlog.push_back(static_cast<int8_t>(E->rcur));
         const long pi = prof_start(E, 5, C);
-        rc = launch_fused(nr, E->pend_comp, a, E->L->tab(), E->tab, C);
+        rc = launch_fused(nr, E->pend_comp ? APPLY_Q : APPLY_F, a, E->L->tab(), E->tab, C);
         prof_stop(E, pi, C);
         if (rc != CDSGD_OK) return rc;
         E->rcur ^= 1;
@@ -1006,7 +1227,7 @@ extern "C" int cdsgd_engine_step(cdsgd_engine* E, const float* g, void* stream) 
         E->rcur ^= 1;
     }
     // 2. exchange round t on the engine's stream (codes are already delivered when fused)
-    E->xused[t & 1] = nr > 1 && !(comp && E->p2p);
+    E->xused[t & 1] = nr > 1 && (!E->p2p || (!comp && !E->pcorr));
     if (E->xused[t & 1]) {
         CUDA_TRY(cudaEventRecord(E->evQ[t & 1], C));
         CUDA_TRY(cudaStreamWaitEvent(E->xs, E->evQ[t & 1], 0));
@@ -1024,11 +1245,23 @@ extern "C" int cdsgd_engine_step(cdsgd_engine* E, const float* g, void* stream) 
     const bool sync_path = !E->uses_local || t < E->n_warmup - 1;
     if (sync_path) {
         if (E->pending) return fail(CDSGD_ERR_STATE, "internal: pending round on the synchronous path");
+        if (!comp && E->p2p && E->pcorr) {
+            rc = p2p_stage(E, t, g, C);
+            if (rc != CDSGD_OK) return rc;
+        }
         rc = engine_apply(E, t, comp, g, nullptr, C);
         if (rc != CDSGD_OK) return rc;
         E->compute_is_loc = false;
     } else {
-        if (E->pending) {
+        bool staged = false;
+        if (E->pending && !comp && E->p2p && E->pcorr && E->pend_comp) {
+            // correction round after a compressed one: K2(t-1) also writes g_t to the stage
+            float* dst = nullptr;
+            P2PArgs xs{};
+            prepare_stage(E, t, &dst, &xs);
+            rc = engine_apply(E, E->pend_t, E->pend_comp, E->pend_grad, g, C, dst, &xs);
+            staged = true;
+        } else if (E->pending) {
             rc = engine_apply(E, E->pend_t, E->pend_comp, E->pend_grad, g, C);
         } else {
             // first local round: loc_{t+1} = W_t - eta_l * g_t (engine.py:380-382, 385-391)
@@ -1038,6 +1271,10 @@ extern "C" int cdsgd_engine_step(cdsgd_engine* E, const float* g, void* stream) 
             prof_stop(E, pi, C);
         }
         if (rc != CDSGD_OK) return rc;
+        if (!comp && E->p2p && E->pcorr && !staged) {  // after apply(t-1) finished writing W: peers may target it
+            rc = p2p_stage(E, t, g, C);
+            if (rc != CDSGD_OK) return rc;
+        }
         E->pending = true;
         E->pend_t = t;
         E->pend_comp = comp;

@@ -212,6 +212,44 @@ __device__ __forceinline__ void p2p_publish(const P2PArgs& x) {
     }
 }
 
+__device__ __forceinline__ void p2p_wait2(const P2PArgs& a, const P2PArgs& b) {
+    // one barrier for both waits (each waits only if armed)
+    if (threadIdx.x == 0) {
+        const P2PArgs* xs[2] = {&a, &b};
+        const long long t0 = clock64();
+        for (int i = 0; i < 2; ++i) {
+            const P2PArgs& x = *xs[i];
+            if (x.nranks <= 0 || x.wait_flags == nullptr || x.wait_value == 0) continue;
+            for (int r = 0; r < x.nranks; ++r)
+                while (ld_acquire_sys(x.wait_flags + r) < x.wait_value) {
+                    __nanosleep(64);
+                    if (clock64() - t0 > (20ll << 30)) {
+                        if (x.err) atomicExch(reinterpret_cast<unsigned long long*>(x.err + 1), EXCHANGE_TIMEOUT);
+                        break;
+                    }
+                }
+        }
+    }
+    __syncthreads();
+}
+
+__device__ __forceinline__ void p2p_publish2(const P2PArgs& a, const P2PArgs& b, unsigned int* counter) {
+    if (a.nranks <= 0 && b.nranks <= 0) return;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence_system();
+        const unsigned prev = atomicAdd(counter, 1u);
+        if (prev == gridDim.x - 1) {
+            __threadfence_system();
+            *counter = 0u;
+            const P2PArgs* xs[2] = {&a, &b};
+            for (int i = 0; i < 2; ++i)
+                for (int r = 0; r < xs[i]->nranks; ++r)
+                    if (xs[i]->publish[r] != nullptr) st_release_sys(xs[i]->publish[r], xs[i]->publish_value);
+        }
+    }
+}
+
 // ================================================================ K1: quantize
 // codec.quantize (codec.py:164-194) per key, fp64 exact:
 //   acc = r + (double)g; plus = acc >= a; minus = acc <= -a;
@@ -402,7 +440,9 @@ struct ApplyQArgs {
     uint64_t* err;
     uint64_t skip_below;
     double* gnorm;
-    P2PArgs x;  // fused exchange: wait for peers' codes, then release the slot
+    P2PArgs x;      // fused exchange: wait for peers' codes, then release the slot
+    float* gstage;  // non-null: also copy g_next here (staging of a P2P correction round)
+    P2PArgs xs;     // staging protocol: wait gfreed, publish gready
 };
 
 __device__ __forceinline__ double apply_mean_general(const uint32_t* codes, int nr, double alpha,
@@ -419,7 +459,7 @@ __device__ __forceinline__ double apply_mean_general(const uint32_t* codes, int 
 
 template <int NR>  // NR > 0: compile-time rank count; NR == 0: runtime (generic)
 __global__ void __launch_bounds__(256) k_apply_quant(ApplyQArgs a, KeyTab kt, DecodeTab tab) {
-    p2p_wait(a.x);
+    p2p_wait2(a.x, a.xs);
     const bool skip = a.err != nullptr && *reinterpret_cast<volatile uint64_t*>(a.err) < a.skip_below;
     __shared__ double s_mean[2 * MAX_RANKS + 1];
     __shared__ float s_upd[2 * MAX_RANKS + 1];
@@ -488,6 +528,7 @@ __global__ void __launch_bounds__(256) k_apply_quant(ApplyQArgs a, KeyTab kt, De
                     }
                     st_stream(a.W + e, w4[0], w4[1], w4[2], w4[3]);
                     if (do_loc) st_stream(a.loc + e, l4[0], l4[1], l4[2], l4[3]);
+                    if (a.gstage != nullptr) st_stream(a.gstage + e, g4[0], g4[1], g4[2], g4[3]);
                 }
             } else {
                 // generic path: lane l owns element 32s + l; word (2s + l/16), code l%16
@@ -520,6 +561,7 @@ __global__ void __launch_bounds__(256) k_apply_quant(ApplyQArgs a, KeyTab kt, De
                         const float wn = __fsub_rn(a.W[e], upd);
                         a.W[e] = wn;
                         if (do_loc) a.loc[e] = __fmaf_rn(-a.eta_l, a.gnext[e], wn);
+                        if (a.gstage != nullptr) a.gstage[e] = a.gnext[e];
                         if (a.gnorm != nullptr) gsq = __fma_rn(mean, mean, gsq);
                         if (rsv) bad_idx = static_cast<uint64_t>(e) < bad_idx ? static_cast<uint64_t>(e) : bad_idx;
                     }
@@ -538,7 +580,7 @@ __global__ void __launch_bounds__(256) k_apply_quant(ApplyQArgs a, KeyTab kt, De
         if (lane == 0 && bad_idx != NO_ERR)
             atomicMin(reinterpret_cast<unsigned long long*>(a.err + 1), static_cast<unsigned long long>(bad_idx));
     }
-    p2p_publish(a.x);
+    p2p_publish2(a.x, a.xs, a.x.counter != nullptr ? a.x.counter : a.xs.counter);
 }
 
 // ================================================================ dequantize / aggregate

@@ -1,0 +1,176 @@
+// kernels_corr.cuh — correction rounds over NVLink without NCCL (fused exchange mode).
+//
+// Reference semantics (engine.py:252, 255, 511): the k-th round pushes full-precision
+// gradients, the server sums them in ascending worker id in fp64, divides by N and
+// applies W -= eta * mean. Here, with every rank holding a W replica in symmetric
+// memory:
+//   k_stage   (round t)   g_t -> my staging slot; release gready[slot][me] = t+1
+//   k_reduce  (round t+1) for MY shard of elements: acquire all gready, read every
+//             rank's staged g over NVLink, fp64 ascending-rank sum, / N (the
+//             reference's arithmetic), W' = W - eta*mean rounded once to fp32, store
+//             W' into EVERY rank's W replica (NVLink stores); publish gfreed (done
+//             reading the stages), the shard's sum(mean^2) and wdone[me] = t+1
+//   k_wait_sum            acquire all wdone (W' complete everywhere), grad-norm total
+// Per rank this moves 2(N-1)/N * 4n bytes each way over NVLink (a ring all-reduce's
+// volume) but nothing through intermediate HBM FIFOs and no NCCL kernels. The sum
+// is bitwise the reference's, and W replicas stay identical because each shard's
+// W' is computed once and broadcast.
+#pragma once
+#include "kernels.cuh"
+
+namespace cdsgd {
+
+struct StageArgs {
+    const float* g;
+    float* stage;
+    int64_t n;
+    P2PArgs x;  // wait: gfreed[slot][*] (previous use released); publish: gready[slot][me]
+};
+
+__global__ void __launch_bounds__(256) k_stage(StageArgs a) {
+    p2p_wait(a.x);
+    const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t nth = (int64_t)gridDim.x * blockDim.x;
+    const bool vec = aligned_to(a.g, 16) && aligned_to(a.stage, 16);
+    int64_t done = 0;
+    if (vec) {
+        const int64_t nv = a.n / 4;
+        for (int64_t i = tid; i < nv; i += nth) {
+            const float4 v = ld_stream(a.g + 4 * i);
+            st_stream(a.stage + 4 * i, v.x, v.y, v.z, v.w);
+        }
+        done = nv * 4;
+    }
+    for (int64_t i = done + tid; i < a.n; i += nth) a.stage[i] = a.g[i];
+    p2p_publish(a.x);
+}
+
+struct ReduceArgs {
+    const float* stage[MAX_RANKS_P2P];  // rank r's staging slot (mapped)
+    float* Wdst[MAX_RANKS_P2P];         // rank r's W replica (mapped)
+    const float* W;                     // my W replica (read)
+    int64_t s0, s1;                     // my shard [s0, s1)
+    int nranks;
+    double eta_g;
+    double inv_n;                       // 1/N when N is a power of two, else 0 (divide)
+    double* gacc;                       // local accumulator of sum(mean^2) (zeroed by the host)
+    double* gpart_dst[MAX_RANKS_P2P];   // rank r's gpart[me]
+    P2PArgs xa;                         // wait: gready[slot][*] >= t+1; publish: gfreed[slot][me]
+    P2PArgs xb;                         // publish: wdone[me]
+};
+
+template <int NR>
+__device__ __forceinline__ float reduce_apply1(const float (&g)[NR], float w, double eta, double inv_n, double& msq) {
+    double tot = static_cast<double>(g[0]);
+#pragma unroll
+    for (int r = 1; r < NR; ++r) tot = __dadd_rn(tot, static_cast<double>(g[r]));   // engine.py:250-253
+    const double mean = inv_n != 0.0 ? __dmul_rn(tot, inv_n) : __ddiv_rn(tot, static_cast<double>(NR));
+    msq = __fma_rn(mean, mean, msq);
+    return __double2float_rn(__dsub_rn(static_cast<double>(w), __dmul_rn(eta, mean)));  // engine.py:511
+}
+
+template <int NR>
+__global__ void __launch_bounds__(256) k_reduce(ReduceArgs a) {
+    p2p_wait(a.xa);
+    const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t nth = (int64_t)gridDim.x * blockDim.x;
+    const int64_t len = a.s1 - a.s0;
+    double msq = 0.0;
+    bool vec = aligned_to(a.W + a.s0, 16);
+#pragma unroll
+    for (int r = 0; r < NR; ++r) vec = vec && aligned_to(a.stage[r] + a.s0, 16) && aligned_to(a.Wdst[r] + a.s0, 16);
+    int64_t done = 0;
+    if (vec) {
+        // U float4 positions per thread per iteration, every (remote) load issued before any use
+        constexpr int U = NR <= 4 ? 4 : 2;
+        const int64_t nv = len / 4;
+        int64_t i = tid;
+        for (; i + (U - 1) * nth < nv; i += U * nth) {
+            float4 gv[U][NR];
+            float4 wv[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int64_t e = a.s0 + 4 * (i + u * nth);
+#pragma unroll
+                for (int r = 0; r < NR; ++r) gv[u][r] = *reinterpret_cast<const float4*>(a.stage[r] + e);  // NVLink
+                wv[u] = ld_stream(a.W + e);
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int64_t e = a.s0 + 4 * (i + u * nth);
+                float g0[NR], g1[NR], g2[NR], g3[NR];
+#pragma unroll
+                for (int r = 0; r < NR; ++r) {
+                    g0[r] = gv[u][r].x; g1[r] = gv[u][r].y; g2[r] = gv[u][r].z; g3[r] = gv[u][r].w;
+                }
+                float4 o;
+                o.x = reduce_apply1<NR>(g0, wv[u].x, a.eta_g, a.inv_n, msq);
+                o.y = reduce_apply1<NR>(g1, wv[u].y, a.eta_g, a.inv_n, msq);
+                o.z = reduce_apply1<NR>(g2, wv[u].z, a.eta_g, a.inv_n, msq);
+                o.w = reduce_apply1<NR>(g3, wv[u].w, a.eta_g, a.inv_n, msq);
+#pragma unroll
+                for (int r = 0; r < NR; ++r) *reinterpret_cast<float4*>(a.Wdst[r] + e) = o;  // NVLink stores
+            }
+        }
+        for (; i < nv; i += nth) {
+            const int64_t e = a.s0 + 4 * i;
+            float4 gv[NR];
+#pragma unroll
+            for (int r = 0; r < NR; ++r) gv[r] = *reinterpret_cast<const float4*>(a.stage[r] + e);
+            const float4 wv = ld_stream(a.W + e);
+            float g0[NR], g1[NR], g2[NR], g3[NR];
+#pragma unroll
+            for (int r = 0; r < NR; ++r) { g0[r] = gv[r].x; g1[r] = gv[r].y; g2[r] = gv[r].z; g3[r] = gv[r].w; }
+            float4 o;
+            o.x = reduce_apply1<NR>(g0, wv.x, a.eta_g, a.inv_n, msq);
+            o.y = reduce_apply1<NR>(g1, wv.y, a.eta_g, a.inv_n, msq);
+            o.z = reduce_apply1<NR>(g2, wv.z, a.eta_g, a.inv_n, msq);
+            o.w = reduce_apply1<NR>(g3, wv.w, a.eta_g, a.inv_n, msq);
+#pragma unroll
+            for (int r = 0; r < NR; ++r) *reinterpret_cast<float4*>(a.Wdst[r] + e) = o;
+        }
+        done = 4 * nv;
+    }
+    for (int64_t i = done + tid; i < len; i += nth) {
+        const int64_t e = a.s0 + i;
+        float g[NR];
+#pragma unroll
+        for (int r = 0; r < NR; ++r) g[r] = a.stage[r][e];
+        const float o = reduce_apply1<NR>(g, a.W[e], a.eta_g, a.inv_n, msq);
+#pragma unroll
+        for (int r = 0; r < NR; ++r) a.Wdst[r][e] = o;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) msq += __shfl_xor_sync(FULL, msq, o);
+    if ((threadIdx.x & 31) == 0 && msq != 0.0) atomicAdd(a.gacc, msq);
+    // last CTA: broadcast the shard's sum(mean^2), then release gfreed and wdone
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence_system();
+        const unsigned prev = atomicAdd(a.xa.counter, 1u);
+        if (prev == gridDim.x - 1) {
+            __threadfence_system();
+            *a.xa.counter = 0u;
+            const double total = *reinterpret_cast<volatile double*>(a.gacc);
+            for (int r = 0; r < a.nranks; ++r) *reinterpret_cast<volatile double*>(a.gpart_dst[r]) = total;
+            __threadfence_system();
+            for (int r = 0; r < a.nranks; ++r) {
+                if (a.xa.publish[r] != nullptr) st_release_sys(a.xa.publish[r], a.xa.publish_value);
+                if (a.xb.publish[r] != nullptr) st_release_sys(a.xb.publish[r], a.xb.publish_value);
+            }
+        }
+    }
+}
+
+// One thread: acquire flags (W' shards of every rank have landed), then optionally
+// total the per-shard sum(mean^2) into the round's grad-norm slot.
+__global__ void k_wait_sum(P2PArgs x, const double* gpart, int n, double* out) {
+    p2p_wait(x);
+    if (threadIdx.x == 0 && out != nullptr) {
+        double s = 0.0;
+        for (int r = 0; r < n; ++r) s += *reinterpret_cast<const volatile double*>(gpart + r);
+        *out = s;
+    }
+}
+
+}  // namespace cdsgd

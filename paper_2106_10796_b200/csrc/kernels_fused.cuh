@@ -18,7 +18,7 @@
 
 namespace cdsgd {
 
-enum { APPLY_Q = 0, APPLY_F = 1 };
+enum { APPLY_Q = 0, APPLY_F = 1, APPLY_L = 2 };  // L: loc = W - eta_l*g only (W already final)
 
 struct FusedArgs {
     // quantize(t)
@@ -52,44 +52,6 @@ struct FusedSmem {
     static constexpr int WARP = S * SLOT;
     static constexpr int BYTES = WARPS * WARP + WARPS * S * 8;
 };
-
-__device__ __forceinline__ void p2p_wait2(const P2PArgs& a, const P2PArgs& b) {
-    // one barrier for both waits (each waits only if armed)
-    if (threadIdx.x == 0) {
-        const P2PArgs* xs[2] = {&a, &b};
-        const long long t0 = clock64();
-        for (int i = 0; i < 2; ++i) {
-            const P2PArgs& x = *xs[i];
-            if (x.nranks <= 0 || x.wait_flags == nullptr || x.wait_value == 0) continue;
-            for (int r = 0; r < x.nranks; ++r)
-                while (ld_acquire_sys(x.wait_flags + r) < x.wait_value) {
-                    __nanosleep(64);
-                    if (clock64() - t0 > (20ll << 30)) {
-                        if (x.err) atomicExch(reinterpret_cast<unsigned long long*>(x.err + 1), EXCHANGE_TIMEOUT);
-                        break;
-                    }
-                }
-        }
-    }
-    __syncthreads();
-}
-
-__device__ __forceinline__ void p2p_publish2(const P2PArgs& a, const P2PArgs& b, unsigned int* counter) {
-    if (a.nranks <= 0 && b.nranks <= 0) return;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        __threadfence_system();
-        const unsigned prev = atomicAdd(counter, 1u);
-        if (prev == gridDim.x - 1) {
-            __threadfence_system();
-            *counter = 0u;
-            const P2PArgs* xs[2] = {&a, &b};
-            for (int i = 0; i < 2; ++i)
-                for (int r = 0; r < xs[i]->nranks; ++r)
-                    if (xs[i]->publish[r] != nullptr) st_release_sys(xs[i]->publish[r], xs[i]->publish_value);
-        }
-    }
-}
 
 template <int NR, int APPLY, int WARPS, int S>
 __global__ void __launch_bounds__(WARPS * 32, 1) k_fused(FusedArgs a, KeyTab kt, DecodeTab tab) {
@@ -393,7 +355,7 @@ __global__ void __launch_bounds__(256, 2) k_fused_ldg(FusedArgs a, KeyTab kt, De
             const int nw = nw64 < TILE_WORDS ? static_cast<int>(nw64) : TILE_WORDS;
             const bool fast = ne == TILE_ELEMS && aligned_to(a.g + e0, 16) && aligned_to(a.r_in + e0, 32) &&
                               aligned_to(a.r_out + e0, 32) && aligned_to(a.W + e0, 16) && aligned_to(a.loc + e0, 16) &&
-                              (APPLY == APPLY_Q || aligned_to(a.gsum + e0, 16));
+                              (APPLY != APPLY_F || aligned_to(a.gsum + e0, 16));
             uint32_t myword = 0;
             if (fast) {
                 float4 gv[CHUNKS], wv[CHUNKS], sv[CHUNKS];
@@ -438,7 +400,7 @@ __global__ void __launch_bounds__(256, 2) k_fused_ldg(FusedArgs a, KeyTab kt, De
                                 const int q = __ffs((cnt.rsv >> (2 * jb)) & 0x55u) / 2;
                                 bad_sym = static_cast<uint64_t>(e + q) < bad_sym ? static_cast<uint64_t>(e + q) : bad_sym;
                             }
-                        } else {
+                        } else if constexpr (APPLY == APPLY_F) {
                             const float s4[4] = {sv[c].x, sv[c].y, sv[c].z, sv[c].w};
 #pragma unroll
                             for (int q = 0; q < 4; ++q) {
@@ -449,8 +411,11 @@ __global__ void __launch_bounds__(256, 2) k_fused_ldg(FusedArgs a, KeyTab kt, De
                                     gsq = __fma_rn(m, m, gsq);
                                 }
                             }
+                        } else {
+#pragma unroll
+                            for (int q = 0; q < 4; ++q) l4[q] = __fmaf_rn(-a.eta_l, g4[q], w4[q]);
                         }
-                        st_stream(a.W + e, w4[0], w4[1], w4[2], w4[3]);
+                        if constexpr (APPLY != APPLY_L) st_stream(a.W + e, w4[0], w4[1], w4[2], w4[3]);
                         st_stream(a.loc + e, l4[0], l4[1], l4[2], l4[3]);
                     }
                     if (!q_off) {
@@ -515,12 +480,14 @@ __global__ void __launch_bounds__(256, 2) k_fused_ldg(FusedArgs a, KeyTab kt, De
                                 wn = __fsub_rn(a.W[e], s_upd[cn + NR]);
                                 isq += cn * cn;
                                 if (rsv) bad_sym = static_cast<uint64_t>(e) < bad_sym ? static_cast<uint64_t>(e) : bad_sym;
-                            } else {
+                            } else if constexpr (APPLY == APPLY_F) {
                                 const float sv1 = a.gsum[e];
                                 wn = __fmaf_rn(-a.scale, sv1, a.W[e]);
                                 if (a.gnorm != nullptr) { const double mm = sv1 * a.inv_n; gsq = __fma_rn(mm, mm, gsq); }
+                            } else {
+                                wn = a.W[e];
                             }
-                            a.W[e] = wn;
+                            if constexpr (APPLY != APPLY_L) a.W[e] = wn;
                             a.loc[e] = __fmaf_rn(-a.eta_l, gval, wn);
                         }
                         if (!q_off) {

@@ -110,24 +110,27 @@ class CDSGDWorker:
             )
             self._eng = out
             self.exchange = exchange if self.world > 1 else "local"
-            if self.world > 1 and exchange == "p2p":
-                self._attach_p2p(group)
+            if self.world > 1 and exchange in ("p2p", "p2p-exact"):
+                self._attach_p2p(group, exact=exchange == "p2p-exact")
             elif self.world > 1 and exchange != "nccl":
-                raise ConfigError(f"exchange must be 'p2p' or 'nccl', got {exchange!r}")
+                raise ConfigError(f"exchange must be 'p2p', 'p2p-exact' or 'nccl', got {exchange!r}")
         self._keep: list[torch.Tensor] = []  # gradients still read by in-flight rounds
         self.check_every = int(check_every)
         self._since_check = 0
         self._lib = _lib.lib()
 
-    def _attach_p2p(self, group) -> None:
+    def _attach_p2p(self, group, exact: bool = False) -> None:
         """Fused NVLink exchange: one symmetric buffer per rank (torch symmetric memory maps
         every peer's buffer into this process); K1 stores codes straight into all ranks'
-        slots and K2 synchronises on release/acquire flags (cdsgd_engine_attach_p2p)."""
+        slots and K2 synchronises on release/acquire flags (cdsgd_engine_attach_p2p).
+        exact=True also replaces the correction all-reduce by the sharded fp64 NVLink reduce."""
         import torch.distributed as dist
         import torch.distributed._symmetric_memory as symm_mem
 
         lib = _lib.lib()
-        nbytes = int(lib.cdsgd_p2p_bytes(self.world, self.layout.n_words))
+        n, nw = self.layout.total, self.layout.n_words
+        nbytes = int(lib.cdsgd_p2p_bytes(self.world, n, nw))
+        w_off = int(lib.cdsgd_p2p_weights_offset(self.world, n, nw))
         grp = group if group is not None else dist.group.WORLD
         self._symm = symm_mem.empty(nbytes, dtype=torch.uint8, device=self.device)
         self._symm.zero_()
@@ -137,7 +140,10 @@ class CDSGDWorker:
         if len(ptrs) != self.world:
             raise ConfigError("symmetric memory group does not match hp.workers")
         arr = (C.c_void_p * self.world)(*ptrs)
-        _lib.check(lib.cdsgd_engine_attach_p2p(self._eng, arr, self.world), "cdsgd_engine_attach_p2p")
+        _lib.check(lib.cdsgd_engine_attach_p2p(self._eng, arr, self.world, int(exact)), "cdsgd_engine_attach_p2p")
+        # the engine moved the W replica into the symmetric buffer (peers write W' shards into it)
+        self.W = self._symm[w_off:w_off + 4 * n].view(torch.float32)
+        torch.cuda.synchronize(self.device)
         dist.barrier(group=grp)  # every rank's flags are zero before any rank's first K1
 
     # ------------------------------------------------------------------ state
@@ -230,9 +236,10 @@ class CDSGDWorker:
 
     def profile_end(self) -> dict:
         """Per-kernel-class total ms and launch counts since profile_begin()."""
-        out = (C.c_double * 12)()
+        out = (C.c_double * 18)()
         _lib.check(self._lib.cdsgd_engine_profile_end(self._eng, out), "profile_end")
-        names = ("quantize", "apply_quant", "apply_full", "local_update", "exchange", "fused")
+        names = ("quantize", "apply_quant", "apply_full", "local_update", "exchange", "fused", "stage", "reduce",
+                 "wait")
         return {nm: {"ms": out[2 * i], "n": int(out[2 * i + 1])} for i, nm in enumerate(names)}
 
     def close(self) -> None:

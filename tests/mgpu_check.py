@@ -78,7 +78,7 @@ def main():
     dist.init_process_group("nccl", device_id=dev)
     _lib.load()
     comm = Comm(share_unique_id(rank), world, rank)
-    exchanges = sys.argv[1:] or ["p2p", "nccl"]
+    exchanges = sys.argv[1:] or ["p2p", "p2p-exact", "nccl"]
     for exchange in exchanges:
         for case in CASES:
             run_case(case, exchange, comm, rank, world, dev)
