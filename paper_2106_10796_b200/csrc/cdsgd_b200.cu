@@ -674,6 +674,7 @@ struct cdsgd_engine {
     int pend_slot = 0;                 // staging slot of the pending correction round
     int64_t s0 = 0, s1 = 0;            // this rank's shard of elements
     double* gacc = nullptr;            // shard sum(mean^2) accumulator
+    unsigned int* sched = nullptr;     // [2] dynamic tile scheduler of the fused kernel
     bool fuse = false;                 // apply(t-1) + quantize(t) in one kernel (N=1 or P2P)
     bool pcorr = false;                // P2P mode: correction rounds by the exact sharded NVLink reduce
     // profiling: event pairs per kernel class (0 quant, 1 apply_q, 2 apply_f, 3 local, 4 exchange, 5 fused,
@@ -900,6 +901,12 @@ extern "C" int cdsgd_engine_create(const cdsgd_engine_desc* d, const cdsgd_layou
     {
         const char* nf = getenv("CDSGD_NO_FUSE");
         E->fuse = d->nranks == 1 && !(nf != nullptr && nf[0] == '1') && !use_ldg();
+        const char* ns = getenv("CDSGD_STATIC_SCHED");
+        if (!(ns != nullptr && ns[0] == '1')) {
+            if (cudaMalloc(&E->sched, 2 * sizeof(unsigned int)) != cudaSuccess ||
+                cudaMemset(E->sched, 0, 2 * sizeof(unsigned int)) != cudaSuccess)
+                E->sched = nullptr;
+        }
     }
     cudaError_t e = cudaSuccess;
     if (d->nranks > 1) {
@@ -1046,6 +1053,7 @@ extern "C" int cdsgd_engine_destroy(cdsgd_engine* E) {
     if (E->xs) cudaStreamDestroy(E->xs);
     if (E->counters) cudaFree(E->counters);
     if (E->gacc) cudaFree(E->gacc);
+    if (E->sched) cudaFree(E->sched);
     delete E;
     return CDSGD_OK;
 }
@@ -1092,6 +1100,7 @@ extern "C" int cdsgd_engine_step(cdsgd_engine* E, const float* g, void* stream) 
             a.eta_l = static_cast<float>(E->d.eta_local);
             a.skip_below = 0;
             a.err = E->d.err;
+            a.sched = E->sched;
             a.xq.nranks = nr;
             for (int r = 0; r < nr; ++r) {
                 a.xq.dst[r] = reinterpret_cast<uint32_t*>(E->peer[r] + E->off_slot[p]) + static_cast<int64_t>(E->d.rank) * nw;
@@ -1150,6 +1159,7 @@ extern "C" int cdsgd_engine_step(cdsgd_engine* E, const float* g, void* stream) 
         const int64_t rel = pnd - E->err_base + 1;
         a.skip_below = rel <= 0 ? 0ull : (static_cast<uint64_t>(rel) << CDSGD_INDEX_BITS);
         a.err = E->d.err;
+        a.sched = E->sched;
         if (E->d.gnorm_sq != nullptr && E->d.gnorm_ring > 0) {
             a.gnorm = E->d.gnorm_sq + (pnd % E->d.gnorm_ring);
             CUDA_TRY(cudaMemsetAsync(a.gnorm, 0, sizeof(double), C));

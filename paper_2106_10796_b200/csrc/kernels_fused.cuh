@@ -42,6 +42,7 @@ struct FusedArgs {
     uint64_t* err;
     P2PArgs xq;  // exchange of round t's codes (wait: slot freed; publish: ready)
     P2PArgs xa;  // exchange of round t-1's codes (wait: ready; publish: freed)
+    unsigned int* sched;  // [2] dynamic tile scheduler {next tile, CTAs done}; nullptr = static ranges
 };
 
 template <int NR, int APPLY, int WARPS, int S>
@@ -341,10 +342,34 @@ __global__ void __launch_bounds__(256, 2) k_fused_ldg(FusedArgs a, KeyTab kt, De
     uint64_t bad_idx = NO_ERR, bad_sym = NO_ERR;
     double gsq = 0.0;
     int isq = 0;
+    // Dynamic schedule: warps claim CLAIM consecutive tiles at a time from a global ticket,
+    // so the kernel ends when the work does, not when the slowest static range does.
+    constexpr int CLAIM = 2;
+    const bool dyn = a.sched != nullptr;
+    int64_t cbase = 0, cend = 0;
+    if (dyn) {
+        unsigned t0 = 0;
+        if (lane == 0) t0 = atomicAdd(a.sched, static_cast<unsigned>(CLAIM));
+        cbase = __shfl_sync(FULL, t0, 0);
+        cend = cbase + CLAIM < kt.ntiles ? cbase + CLAIM : kt.ntiles;
+        tb = cbase;
+        te = cbase < kt.ntiles ? kt.ntiles : cbase;  // loop bound; real bound checked per claim
+    }
     if (tb < te) {
         TileCursor cc;
         cc.seek(kt, tb);
         for (int64_t ti = tb; ti < te; ++ti) {
+            if (dyn) {
+                if (ti >= cend) {  // claim the next batch
+                    unsigned t0 = 0;
+                    if (lane == 0) t0 = atomicAdd(a.sched, static_cast<unsigned>(CLAIM));
+                    const int64_t nb = __shfl_sync(FULL, t0, 0);
+                    if (nb >= kt.ntiles) break;
+                    ti = nb;
+                    cend = nb + CLAIM < kt.ntiles ? nb + CLAIM : kt.ntiles;
+                    if (ti < cc.t0) cc.seek(kt, ti);
+                }
+            }
             cc.advance_to(kt, ti);
             const int64_t j = ti - cc.t0;
             const int64_t e0 = cc.e0 + j * TILE_ELEMS;
@@ -531,6 +556,17 @@ __global__ void __launch_bounds__(256, 2) k_fused_ldg(FusedArgs a, KeyTab kt, De
             atomicMin(reinterpret_cast<unsigned long long*>(a.err), static_cast<unsigned long long>(bad_idx));
         if (lane == 0 && bad_sym != NO_ERR)
             atomicMin(reinterpret_cast<unsigned long long*>(a.err + 1), static_cast<unsigned long long>(bad_sym));
+    }
+    if (dyn) {  // the last CTA out resets the ticket for the next launch on this stream
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            if (atomicAdd(a.sched + 1, 1u) == gridDim.x - 1) {
+                a.sched[0] = 0u;
+                a.sched[1] = 0u;
+                __threadfence();
+            }
+        }
     }
     p2p_publish2(a.xq, a.xa, a.xq.counter != nullptr ? a.xq.counter : a.xa.counter);
 }
