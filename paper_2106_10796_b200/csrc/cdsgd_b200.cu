@@ -423,7 +423,7 @@ int launch_apply_quant(const cdsgd_layout* L, float* W, const uint32_t* gathered
                        double alpha, double eta_g, const float* gnext, float* loc, double eta_l, uint64_t* err,
                        uint64_t skip_below, double* gnorm, const DecodeTab* tab_in, int exact_in,
                        cudaStream_t st, const P2PArgs* x = nullptr, float* gstage = nullptr,
-                       const P2PArgs* xs = nullptr) {
+                       const P2PArgs* xs = nullptr, unsigned int* sched = nullptr) {
     if (L == nullptr) return fail(CDSGD_ERR_ARG, "layout is NULL");
     if (nr < 1 || nr > MAX_RANKS - 1) return fail(CDSGD_ERR_ARG, "nranks must be in [1, %d]", MAX_RANKS - 1);
     if ((gnext == nullptr) != (loc == nullptr)) return fail(CDSGD_ERR_ARG, "g_next and loc_out go together");
@@ -446,6 +446,7 @@ int launch_apply_quant(const cdsgd_layout* L, float* W, const uint32_t* gathered
     a.x = x != nullptr ? *x : P2PArgs{};
     a.gstage = gstage;
     a.xs = xs != nullptr ? *xs : P2PArgs{};
+    a.sched = sched;
     DecodeTab tab;
     int exact;
     if (tab_in != nullptr) {
@@ -674,7 +675,7 @@ struct cdsgd_engine {
     int pend_slot = 0;                 // staging slot of the pending correction round
     int64_t s0 = 0, s1 = 0;            // this rank's shard of elements
     double* gacc = nullptr;            // shard sum(mean^2) accumulator
-    unsigned int* sched = nullptr;     // [2] dynamic tile scheduler of the fused kernel
+    unsigned int* sched = nullptr;     // [4] dynamic tile schedulers: fused kernel [0,1], K2 [2,3]
     bool fuse = false;                 // apply(t-1) + quantize(t) in one kernel (N=1 or P2P)
     bool pcorr = false;                // P2P mode: correction rounds by the exact sharded NVLink reduce
     // profiling: event pairs per kernel class (0 quant, 1 apply_q, 2 apply_f, 3 local, 4 exchange, 5 fused,
@@ -859,7 +860,8 @@ int engine_apply(cdsgd_engine* E, int64_t p, bool comp, const float* gp, const f
         const long pi = prof_start(E, 1, C);
         const int rc = launch_apply_quant(E->L, E->d.weights, E->d.gathered[p & 1], nr, words_of(E), E->d.alpha,
                                           E->d.eta_global, gnext, loc, E->d.eta_local, E->d.err, skip_below, gn,
-                                          &E->tab, E->exact, C, &x, gstage, xs);
+                                          &E->tab, E->exact, C, &x, gstage, xs,
+                                          E->sched != nullptr ? E->sched + 2 : nullptr);
         prof_stop(E, pi, C);
         return rc;
     }
@@ -903,8 +905,8 @@ extern "C" int cdsgd_engine_create(const cdsgd_engine_desc* d, const cdsgd_layou
         E->fuse = d->nranks == 1 && !(nf != nullptr && nf[0] == '1') && !use_ldg();
         const char* ns = getenv("CDSGD_STATIC_SCHED");
         if (!(ns != nullptr && ns[0] == '1')) {
-            if (cudaMalloc(&E->sched, 2 * sizeof(unsigned int)) != cudaSuccess ||
-                cudaMemset(E->sched, 0, 2 * sizeof(unsigned int)) != cudaSuccess)
+            if (cudaMalloc(&E->sched, 4 * sizeof(unsigned int)) != cudaSuccess ||
+                cudaMemset(E->sched, 0, 4 * sizeof(unsigned int)) != cudaSuccess)
                 E->sched = nullptr;
         }
     }

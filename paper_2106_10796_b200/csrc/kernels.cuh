@@ -443,6 +443,7 @@ struct ApplyQArgs {
     P2PArgs x;      // fused exchange: wait for peers' codes, then release the slot
     float* gstage;  // non-null: also copy g_next here (staging of a P2P correction round)
     P2PArgs xs;     // staging protocol: wait gfreed, publish gready
+    unsigned int* sched;  // [2] dynamic tile scheduler {next tile, CTAs done}; nullptr = static ranges
 };
 
 __device__ __forceinline__ double apply_mean_general(const uint32_t* codes, int nr, double alpha,
@@ -476,10 +477,28 @@ __global__ void __launch_bounds__(256) k_apply_quant(ApplyQArgs a, KeyTab kt, De
     int isq = 0;  // sum of cnt^2 on the table path: gsq += isq * (alpha/N)^2
     uint64_t bad_idx = NO_ERR;
     const bool do_loc = a.loc != nullptr;
+    constexpr int CLAIM = 2;
+    const bool dyn = a.sched != nullptr;
+    int64_t cend = 0;
+    if (dyn) {  // warps claim CLAIM tiles at a time from a global ticket (see k_fused_ldg)
+        unsigned t0 = 0;
+        if (lane == 0) t0 = atomicAdd(a.sched, static_cast<unsigned>(CLAIM));
+        tb = __shfl_sync(FULL, t0, 0);
+        cend = tb + CLAIM < kt.ntiles ? tb + CLAIM : kt.ntiles;
+        te = tb < kt.ntiles ? kt.ntiles : tb;
+    }
     if (tb < te && !skip) {
         TileCursor kc;
         kc.seek(kt, tb);
         for (int64_t ti = tb; ti < te; ++ti) {
+            if (dyn && ti >= cend) {
+                unsigned t0 = 0;
+                if (lane == 0) t0 = atomicAdd(a.sched, static_cast<unsigned>(CLAIM));
+                const int64_t nb = __shfl_sync(FULL, t0, 0);
+                if (nb >= kt.ntiles) break;
+                ti = nb;
+                cend = nb + CLAIM < kt.ntiles ? nb + CLAIM : kt.ntiles;
+            }
             kc.advance_to(kt, ti);
             const int64_t j = ti - kc.t0;
             const int64_t e0 = kc.e0 + j * TILE_ELEMS;
@@ -579,6 +598,17 @@ __global__ void __launch_bounds__(256) k_apply_quant(ApplyQArgs a, KeyTab kt, De
         bad_idx = warp_min_u64(bad_idx);
         if (lane == 0 && bad_idx != NO_ERR)
             atomicMin(reinterpret_cast<unsigned long long*>(a.err + 1), static_cast<unsigned long long>(bad_idx));
+    }
+    if (dyn) {  // last CTA out resets the ticket (skipped CTAs still count)
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            if (atomicAdd(a.sched + 1, 1u) == gridDim.x - 1) {
+                a.sched[0] = 0u;
+                a.sched[1] = 0u;
+                __threadfence();
+            }
+        }
     }
     p2p_publish2(a.x, a.xs, a.x.counter != nullptr ? a.x.counter : a.xs.counter);
 }
