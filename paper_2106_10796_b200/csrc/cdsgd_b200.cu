@@ -131,25 +131,9 @@ int tma_cfg() {
     static const int v = read_cfg("CDSGD_TMA_CFG", 162);
     return v;
 }
-int tma_cfg2() {
+int tma_cfg2() {  // K3
     static const int v = read_cfg("CDSGD_TMA_CFG2", 84);
     return v;
-}
-template <int NR, int WP, int ST>
-int launch_aq_tma(const ApplyQArgs& a, const KeyTab& kt, const DecodeTab& tab, cudaStream_t st) {
-    using SM = ApplyQSmem<NR, WP, ST>;
-    static_assert(SM::BYTES <= 227 * 1024, "smem");
-    if (!prepare_tma(k_apply_quant_tma<NR, WP, ST>, SM::BYTES)) return fail(CDSGD_ERR_CUDA, "smem attribute");
-    k_apply_quant_tma<NR, WP, ST><<<tma_grid(kt.ntiles, WP), WP * 32, SM::BYTES, st>>>(a, kt, tab);
-    return CDSGD_OK;
-}
-template <int NR>
-int launch_aq_tma_cfg(const ApplyQArgs& a, const KeyTab& kt, const DecodeTab& tab, cudaStream_t st) {
-    switch (tma_cfg2()) {
-        case 162: return launch_aq_tma<NR, 16, 2>(a, kt, tab, st);
-        case 83: return launch_aq_tma<NR, 8, 3>(a, kt, tab, st);
-        default: return launch_aq_tma<NR, 8, 4>(a, kt, tab, st);
-    }
 }
 template <int WP, int ST>
 int launch_af_tma(const ApplyFArgs& a, cudaStream_t st) {
@@ -458,20 +442,6 @@ int launch_apply_quant(const cdsgd_layout* L, float* W, const uint32_t* gathered
     }
     a.exact = exact;
     const KeyTab kt = L->tab();
-    static const bool k2_tma = [] {
-        const char* e = getenv("CDSGD_K2_TMA");
-        return e != nullptr && e[0] == '1';
-    }();
-    if (k2_tma && exact && nr <= 8 && a.x.nranks == 0 && gstage == nullptr) {
-        int rc = CDSGD_OK;
-#define AQT(R)                                               \
-    case R: rc = launch_aq_tma_cfg<R>(a, kt, tab, st); break;
-        switch (nr) { AQT(1) AQT(2) AQT(3) AQT(4) AQT(5) AQT(6) AQT(7) AQT(8) }
-        if (rc != CDSGD_OK) return rc;
-#undef AQT
-        LAUNCH_CHECK();
-        return CDSGD_OK;
-    }
 #define AQ(R)                                                                                   \
     case R:                                                                                     \
         k_apply_quant<R><<<tile_grid(k_apply_quant<R>, kt.ntiles), THREADS, 0, st>>>(a, kt, tab); \

@@ -1,4 +1,4 @@
-// kernels_tma.cuh — TMA-staged (cp.async.bulk + mbarrier) variants of K1/K2/K3.
+// kernels_tma.cuh — TMA-staged (cp.async.bulk + mbarrier) variants of K1 and K3.
 //
 // Each warp owns a contiguous range of tiles (as in kernels.cuh) and an S-slot
 // ring in shared memory. Lane 0 arms slot s's mbarrier with the tile's byte
@@ -240,204 +240,9 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
     p2p_publish(x);
 }
 
-// ================================================================ K2 (TMA)
-// Slot: W tile (2 KB) | g_next tile (2 KB) | per rank a 16-byte-aligned window
-// (<= 144 B) around the tile's 32 code words.
+// Code window per rank staged by the fused TMA kernel: a 16-byte-aligned window
+// (<= 144 B) around a tile's 32 code words.
 constexpr int CODE_WIN = 144;
-template <int NR, int WARPS, int S>
-struct ApplyQSmem {
-    static constexpr int SLOT = 2 * TILE_ELEMS * 4 + NR * CODE_WIN;
-    static constexpr int WARP = S * SLOT;
-    static constexpr int BYTES = WARPS * WARP + WARPS * S * 8;
-};
-
-template <int NR, int WARPS, int S>
-__global__ void __launch_bounds__(WARPS * 32, 1) k_apply_quant_tma(ApplyQArgs a, KeyTab kt, DecodeTab tab) {
-    using SM = ApplyQSmem<NR, WARPS, S>;
-    extern __shared__ __align__(128) unsigned char smem[];
-    __shared__ double s_mean[2 * MAX_RANKS + 1];
-    __shared__ float s_upd[2 * MAX_RANKS + 1];
-    if (a.err != nullptr && *reinterpret_cast<volatile uint64_t*>(a.err) < a.skip_below) return;
-    if (threadIdx.x < 2 * NR + 1) {
-        s_mean[threadIdx.x] = tab.mean[threadIdx.x];
-        s_upd[threadIdx.x] = tab.upd[threadIdx.x];
-    }
-    __syncthreads();
-    const int warp = threadIdx.x >> 5;
-    const int lane = threadIdx.x & 31;
-    unsigned char* ring = smem + warp * SM::WARP;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + WARPS * SM::WARP) + warp * S;
-    const bool do_loc = a.loc != nullptr;
-    const char* gbase = reinterpret_cast<const char*>(a.gathered);
-    const char* gend = gbase + 4 * (NR * a.stride);
-    int64_t tb, te;
-    warp_range(kt.ntiles, tb, te);
-    double gsq = 0.0;
-    uint64_t bad_idx = NO_ERR;
-    if (tb < te) {
-        if (lane == 0) {
-            for (int s = 0; s < S; ++s) tma::mbar_init(&bars[s], 1);
-            tma::fence_mbar_init();
-        }
-        __syncwarp();
-        TileCursor pc, cc;
-        pc.seek(kt, tb);
-        cc = pc;
-        uint32_t staged = 0, phase = 0;
-        auto issue = [&](int64_t ti, int slot) {
-            pc.advance_to(kt, ti);
-            const int64_t jj = ti - pc.t0;
-            const int64_t e0 = pc.e0 + jj * TILE_ELEMS;
-            const int64_t w0 = pc.w0 + jj * TILE_WORDS;
-            bool ok = a.exact && pc.e1 - e0 >= TILE_ELEMS && aligned_to(a.W + e0, 16) &&
-                      (!do_loc || (aligned_to(a.gnext + e0, 16) && aligned_to(a.loc + e0, 16)));
-            uint32_t bytes = 0;
-            const char* lo[NR];
-            uint32_t len[NR];
-#pragma unroll
-            for (int r = 0; r < NR; ++r) {
-                const char* src = reinterpret_cast<const char*>(a.gathered + r * a.stride + w0);
-                lo[r] = reinterpret_cast<const char*>(reinterpret_cast<uintptr_t>(src) & ~uintptr_t(15));
-                const char* hi = reinterpret_cast<const char*>((reinterpret_cast<uintptr_t>(src) + 4 * TILE_WORDS + 15) &
-                                                               ~uintptr_t(15));
-                len[r] = static_cast<uint32_t>(hi - lo[r]);
-                ok = ok && lo[r] >= gbase && hi <= gend;
-                bytes += len[r];
-            }
-            if (ok) {
-                if (lane == 0) {
-                    unsigned char* sl = ring + slot * SM::SLOT;
-                    bytes += TILE_ELEMS * 4 * (do_loc ? 2 : 1);
-                    tma::arrive_expect_tx(&bars[slot], bytes);
-                    tma::bulk_g2s(sl, a.W + e0, TILE_ELEMS * 4, &bars[slot]);
-                    if (do_loc) tma::bulk_g2s(sl + TILE_ELEMS * 4, a.gnext + e0, TILE_ELEMS * 4, &bars[slot]);
-#pragma unroll
-                    for (int r = 0; r < NR; ++r)
-                        tma::bulk_g2s(sl + 2 * TILE_ELEMS * 4 + r * CODE_WIN, lo[r], len[r], &bars[slot]);
-                }
-                staged |= 1u << slot;
-            } else {
-                staged &= ~(1u << slot);
-            }
-        };
-        for (int i = 0; i < S - 1 && tb + i < te; ++i) issue(tb + i, i);
-        int slot = 0;
-        for (int64_t ti = tb; ti < te; ++ti) {
-            if (ti + S - 1 < te) {
-                __syncwarp();  // every lane is done reading the slot being refilled (WAR; no proxy fence needed)
-                issue(ti + S - 1, slot == 0 ? S - 1 : slot - 1);
-            }
-            cc.advance_to(kt, ti);
-            const int64_t j = ti - cc.t0;
-            const int64_t e0 = cc.e0 + j * TILE_ELEMS;
-            const int64_t w0 = cc.w0 + j * TILE_WORDS;
-            const int64_t ne64 = cc.e1 - e0;
-            const int ne = ne64 < TILE_ELEMS ? static_cast<int>(ne64) : TILE_ELEMS;
-            const int64_t nw64 = cc.w1 - w0;
-            const int nw = nw64 < TILE_WORDS ? static_cast<int>(nw64) : TILE_WORDS;
-            if (staged & (1u << slot)) {
-                tma::wait(&bars[slot], (phase >> slot) & 1u);
-                phase ^= 1u << slot;
-                const unsigned char* sl = ring + slot * SM::SLOT;
-                const float* sW = reinterpret_cast<const float*>(sl);
-                const float* sG = reinterpret_cast<const float*>(sl + TILE_ELEMS * 4);
-                const unsigned char* sc = sl + 2 * TILE_ELEMS * 4;
-                uint32_t off[NR];
-#pragma unroll
-                for (int r = 0; r < NR; ++r)
-                    off[r] = static_cast<uint32_t>(reinterpret_cast<uintptr_t>(a.gathered + r * a.stride + w0) & 15u);
-                // phase A: all smem reads of the tile
-                uint32_t cw[CHUNKS][NR];
-                float w4[CHUNKS][4], g4[CHUNKS][4];
-#pragma unroll
-                for (int c = 0; c < CHUNKS; ++c) {
-                    const int widx = 8 * c + (lane >> 2);
-#pragma unroll
-                    for (int r = 0; r < NR; ++r)
-                        cw[c][r] = *reinterpret_cast<const uint32_t*>(sc + r * CODE_WIN + off[r] + 4 * widx);
-                    tma::lds4(sW + 128 * c, lane, w4[c]);
-                    if (do_loc) tma::lds4(sG + 128 * c, lane, g4[c]);
-                }
-                // phase B: count codes over ranks, table lookup, fp32 update, stores
-                const int jb = 4 * (lane & 3);
-#pragma unroll
-                for (int c = 0; c < CHUNKS; ++c) {
-                    const int64_t e = e0 + 128 * c + 4 * lane;
-                    Counts cnt{0u, 0u, 0u, 0u, 0u};
-#pragma unroll
-                    for (int r = 0; r < NR; ++r) count_add(cnt, cw[c][r]);
-                    float l4[4];
-                    int cq[4];
-                    lane_counts(cnt, lane, cq);
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        w4[c][q] = __fsub_rn(w4[c][q], s_upd[cq[q] + NR]);
-                        if (do_loc) l4[q] = __fmaf_rn(-a.eta_l, g4[c][q], w4[c][q]);
-                        if (a.gnorm != nullptr) {
-                            const double mv = s_mean[cq[q] + NR];
-                            gsq = __fma_rn(mv, mv, gsq);
-                        }
-                    }
-                    if (((cnt.rsv >> (2 * jb)) & 0xffu) != 0u) {
-                        const int q = __ffs((cnt.rsv >> (2 * jb)) & 0x55u) / 2;
-                        const uint64_t idx = static_cast<uint64_t>(e + q);
-                        bad_idx = idx < bad_idx ? idx : bad_idx;
-                    }
-                    st_stream(a.W + e, w4[c][0], w4[c][1], w4[c][2], w4[c][3]);
-                    if (do_loc) st_stream(a.loc + e, l4[0], l4[1], l4[2], l4[3]);
-                }
-            } else {
-                uint32_t wv[NR];
-                const bool wl = lane < nw;
-#pragma unroll
-                for (int r = 0; r < NR; ++r) wv[r] = wl ? a.gathered[r * a.stride + w0 + lane] : 0u;
-#pragma unroll 2
-                for (int s = 0; s < TILE_ELEMS / 32; ++s) {
-                    const int el = 32 * s + lane;
-                    uint32_t codes[NR];
-#pragma unroll
-                    for (int r = 0; r < NR; ++r)
-                        codes[r] = (__shfl_sync(FULL, wv[r], 2 * s + (lane >> 4)) >> (2 * (lane & 15))) & 3u;
-                    if (el < ne) {
-                        const int64_t e = e0 + el;
-                        bool rsv = false;
-                        double mean;
-                        float upd;
-                        if (a.exact) {
-                            int cn = 0;
-#pragma unroll
-                            for (int r = 0; r < NR; ++r) {
-                                rsv |= codes[r] == 3u;
-                                cn += (codes[r] == 1u) - (codes[r] == 2u);
-                            }
-                            mean = s_mean[cn + NR];
-                            upd = s_upd[cn + NR];
-                        } else {
-                            mean = apply_mean_general(codes, NR, a.alpha, a.inv_n_or_zero, rsv);
-                            upd = __double2float_rn(__dmul_rn(a.eta_g_d, mean));
-                        }
-                        const float wn = __fsub_rn(a.W[e], upd);
-                        a.W[e] = wn;
-                        if (do_loc) a.loc[e] = __fmaf_rn(-a.eta_l, a.gnext[e], wn);
-                        if (a.gnorm != nullptr) gsq = __fma_rn(mean, mean, gsq);
-                        if (rsv) bad_idx = static_cast<uint64_t>(e) < bad_idx ? static_cast<uint64_t>(e) : bad_idx;
-                    }
-                }
-            }
-            slot = slot + 1 == S ? 0 : slot + 1;
-        }
-    }
-    if (a.gnorm != nullptr) {
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) gsq += __shfl_xor_sync(FULL, gsq, o);
-        if (lane == 0 && gsq != 0.0) atomicAdd(a.gnorm, gsq);
-    }
-    if (a.err != nullptr) {
-        bad_idx = warp_min_u64(bad_idx);
-        if (lane == 0 && bad_idx != NO_ERR)
-            atomicMin(reinterpret_cast<unsigned long long*>(a.err + 1), static_cast<unsigned long long>(bad_idx));
-    }
-}
 
 // ================================================================ K3 (TMA)
 template <int WARPS, int S>
