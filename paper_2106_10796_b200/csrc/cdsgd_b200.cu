@@ -648,6 +648,7 @@ struct cdsgd_engine {
     unsigned int* sched = nullptr;     // [4] dynamic tile schedulers: fused kernel [0,1], K2 [2,3]
     bool fuse = false;                 // apply(t-1) + quantize(t) in one kernel (N=1 or P2P)
     bool pcorr = false;                // P2P mode: correction rounds by the exact sharded NVLink reduce
+    bool diag_local_codes = false;     // timing diagnostic: store codes only locally
     // profiling: event pairs per kernel class (0 quant, 1 apply_q, 2 apply_f, 3 local, 4 exchange, 5 fused,
     // 6 stage, 7 reduce, 8 wait)
     bool prof = false;
@@ -730,9 +731,21 @@ int p2p_stage(cdsgd_engine* E, int64_t t, const float* g, cudaStream_t C) {
     return CDSGD_OK;
 }
 
+// The reduce runs beside the next round's quantize kernel; one CTA per SM measured best
+// (fewer CTAs starve the remote loads: 64 -> 374 us, 32 -> 578 us at N=4).
+// CDSGD_REDUCE_CTAS overrides (default: number of SMs).
+int reduce_ctas() {
+    static const int v = [] {
+        const char* e = getenv("CDSGD_REDUCE_CTAS");
+        const int x = e != nullptr ? atoi(e) : 0;
+        return x > 0 ? x : dev_info().sms;
+    }();
+    return v;
+}
 template <int NR>
 void launch_reduce_t(const ReduceArgs& a, int64_t len, cudaStream_t C) {
-    k_reduce<NR><<<flat_grid(k_reduce<NR>, (len + 3) / 4), THREADS, 0, C>>>(a);
+    const int grid = std::min(flat_grid(k_reduce<NR>, (len + 3) / 4), reduce_ctas());
+    k_reduce<NR><<<grid, THREADS, 0, C>>>(a);
 }
 
 // Apply correction round p: reduce my shard from every rank's stage, broadcast W',
@@ -792,13 +805,27 @@ int p2p_reduce(cdsgd_engine* E, int64_t p, cudaStream_t C) {
     return CDSGD_OK;
 }
 
+// Start the reduce of correction round t on the exchange stream once this rank's
+// stage is written (recorded on C), so it overlaps the next round's quantize.
+int p2p_reduce_async(cdsgd_engine* E, int64_t t, cudaStream_t C) {
+    CUDA_TRY(cudaEventRecord(E->evQ[t & 1], C));
+    CUDA_TRY(cudaStreamWaitEvent(E->xs, E->evQ[t & 1], 0));
+    const int rc = p2p_reduce(E, t, E->xs);
+    if (rc != CDSGD_OK) return rc;
+    CUDA_TRY(cudaEventRecord(E->evX[t & 1], E->xs));
+    E->xused[t & 1] = true;
+    return CDSGD_OK;
+}
+
 // Finish round p: wait for its exchange, then K2 (codes) or K3 (full) fused with
 // the local update from g_next (nullable).
 int engine_apply(cdsgd_engine* E, int64_t p, bool comp, const float* gp, const float* gnext, cudaStream_t C,
                  float* gstage = nullptr, const P2PArgs* xs = nullptr) {
     const int nr = E->d.nranks;
     if (!comp && E->p2p && E->pcorr) {  // P2P correction: exact sharded reduce, then (optionally) the local update
-        int rc = p2p_reduce(E, p, C);
+        int rc = CDSGD_OK;
+        if (E->xused[p & 1]) CUDA_TRY(cudaStreamWaitEvent(C, E->evX[p & 1], 0));  // reduce already ran on X
+        else rc = p2p_reduce(E, p, C);
         if (rc == CDSGD_OK && gnext != nullptr)
             rc = cdsgd_local_update(E->d.weights, CDSGD_F32, gnext, CDSGD_F32, E->d.loc, CDSGD_F32, E->L->n,
                                     E->d.eta_local, C);
@@ -976,6 +1003,10 @@ extern "C" int cdsgd_engine_attach_p2p(cdsgd_engine* E, void* const* peer_bases,
     E->p2p = true;
     E->pcorr = exact_correction != 0;
     {
+        const char* nr = getenv("CDSGD_DIAG_NO_REMOTE_CODES");  // timing diagnostic only: wrong results
+        E->diag_local_codes = nr != nullptr && nr[0] == '1';
+    }
+    {
         const char* nf = getenv("CDSGD_NO_FUSE");
         E->fuse = !(nf != nullptr && nf[0] == '1');
     }
@@ -1051,61 +1082,51 @@ extern "C" int cdsgd_engine_step(cdsgd_engine* E, const float* g, void* stream) 
     uint32_t* mine = E->d.gathered[t & 1] + static_cast<int64_t>(E->d.rank) * nw;
     const bool sync_path0 = !E->uses_local || t < E->n_warmup - 1;
     if (E->p2p && E->pcorr && E->pending && !E->pend_comp) {
-        // ---- previous round was a P2P correction: W_t = reduce(stage_{t-1}) first
-        rc = p2p_reduce(E, E->pend_t, C);
-        if (rc != CDSGD_OK) return rc;
-        E->pending = false;
+        // ---- previous round was a P2P correction whose reduce runs on stream X:
+        // quantize(t) overlaps it; then loc_{t+1} = W_t - eta_l*g_t once W_t is complete
         E->rlog.push_back(static_cast<int8_t>(E->rcur));
         if (comp) {
-            // quantize(t) + loc_{t+1} = W_t - eta_l*g_t in one pass
             const int p = static_cast<int>(t & 1);
             char* local = E->peer[E->d.rank];
-            FusedArgs a{};
-            a.g = g;
-            a.r_in = E->d.residual[E->rcur];
-            a.r_out = E->d.residual[E->rcur ^ 1];
-            a.words = mine;
-            a.alpha = E->d.alpha;
-            a.tag = static_cast<uint64_t>(t - E->err_base) << CDSGD_INDEX_BITS;
-            a.W = E->d.weights;
-            a.loc = E->d.loc;
-            a.eta_l = static_cast<float>(E->d.eta_local);
-            a.skip_below = 0;
-            a.err = E->d.err;
-            a.sched = E->sched;
-            a.xq.nranks = nr;
+            P2PArgs x{};
+            x.nranks = nr;
             for (int r = 0; r < nr; ++r) {
-                a.xq.dst[r] = reinterpret_cast<uint32_t*>(E->peer[r] + E->off_slot[p]) + static_cast<int64_t>(E->d.rank) * nw;
-                a.xq.publish[r] = reinterpret_cast<uint64_t*>(E->peer[r] + E->off_ready) + p * nr + E->d.rank;
+                x.dst[r] = reinterpret_cast<uint32_t*>(E->peer[E->diag_local_codes ? E->d.rank : r] + E->off_slot[p]) +
+                           static_cast<int64_t>(E->d.rank) * nw;
+                x.publish[r] = reinterpret_cast<uint64_t*>(E->peer[r] + E->off_ready) + p * nr + E->d.rank;
             }
-            a.xq.wait_flags = reinterpret_cast<const uint64_t*>(local + E->off_freed) + p * nr;
-            a.xq.wait_value = E->last_use[p] >= 0 ? static_cast<uint64_t>(E->last_use[p]) + 1 : 0;
-            a.xq.publish_value = static_cast<uint64_t>(t) + 1;
-            a.xq.counter = E->counters;
-            a.xq.err = E->d.err;
-            E->last_use[p] = t;
-            const long pi = prof_start(E, 5, C);
-            rc = launch_fused(nr, APPLY_L, a, E->L->tab(), E->tab, C);
+            x.wait_flags = reinterpret_cast<const uint64_t*>(local + E->off_freed) + p * nr;
+            x.wait_value = E->last_use[p] >= 0 ? static_cast<uint64_t>(E->last_use[p]) + 1 : 0;
+            x.publish_value = static_cast<uint64_t>(t) + 1;
+            x.counter = E->counters;
+            x.err = E->d.err;
+            const uint64_t tag = static_cast<uint64_t>(t - E->err_base) << CDSGD_INDEX_BITS;
+            const long pi = prof_start(E, 0, C);
+            rc = launch_quant_tma_cfg(g, E->d.residual[E->rcur], E->d.residual[E->rcur ^ 1], mine, E->L->tab(),
+                                      E->d.alpha, E->d.err, tag, C, x);
+            if (rc == CDSGD_OK) {
+                g_launches.fetch_add(1, std::memory_order_relaxed);
+                const cudaError_t le = cudaGetLastError();
+                if (le != cudaSuccess) rc = fail(CDSGD_ERR_CUDA, "kernel launch: %s", cudaGetErrorString(le));
+            }
             prof_stop(E, pi, C);
             if (rc != CDSGD_OK) return rc;
+            E->last_use[p] = t;
             E->rcur ^= 1;
-            E->pending = true;
-            E->pend_t = t;
-            E->pend_comp = true;
-            E->pend_grad = g;
-        } else {
-            // another correction round: loc_{t+1} = W_t - eta_l*g_t, then stage g_t
-            rc = cdsgd_local_update(E->d.weights, CDSGD_F32, g, CDSGD_F32, E->d.loc, CDSGD_F32, E->L->n,
-                                    E->d.eta_local, stream);
-            if (rc != CDSGD_OK) return rc;
+        }
+        rc = engine_apply(E, E->pend_t, false, E->pend_grad, g, C);  // wait X, loc = W_t - eta_l*g_t
+        if (rc != CDSGD_OK) return rc;
+        E->xused[t & 1] = false;
+        if (!comp) {  // another correction round: stage g_t and start its reduce on X
             rc = p2p_stage(E, t, g, C);
             if (rc != CDSGD_OK) return rc;
-            E->pending = true;
-            E->pend_t = t;
-            E->pend_comp = false;
-            E->pend_grad = g;
+            rc = p2p_reduce_async(E, t, C);
+            if (rc != CDSGD_OK) return rc;
         }
-        E->xused[t & 1] = false;
+        E->pending = true;
+        E->pend_t = t;
+        E->pend_comp = comp;
+        E->pend_grad = g;
         E->compute_is_loc = true;
         E->t = t + 1;
         return CDSGD_OK;
@@ -1141,7 +1162,8 @@ extern "C" int cdsgd_engine_step(cdsgd_engine* E, const float* g, void* stream) 
             char* local = E->peer[E->d.rank];
             a.xq.nranks = a.xa.nranks = nr;
             for (int r = 0; r < nr; ++r) {
-                a.xq.dst[r] = reinterpret_cast<uint32_t*>(E->peer[r] + E->off_slot[p]) + static_cast<int64_t>(E->d.rank) * nw;
+                a.xq.dst[r] = reinterpret_cast<uint32_t*>(E->peer[E->diag_local_codes ? E->d.rank : r] + E->off_slot[p]) +
+                              static_cast<int64_t>(E->d.rank) * nw;
                 a.xq.publish[r] = reinterpret_cast<uint64_t*>(E->peer[r] + E->off_ready) + p * nr + E->d.rank;
                 a.xa.publish[r] = reinterpret_cast<uint64_t*>(E->peer[r] + E->off_freed) + q * nr + E->d.rank;
             }
@@ -1255,6 +1277,10 @@ extern "C" int cdsgd_engine_step(cdsgd_engine* E, const float* g, void* stream) 
         if (rc != CDSGD_OK) return rc;
         if (!comp && E->p2p && E->pcorr && !staged) {  // after apply(t-1) finished writing W: peers may target it
             rc = p2p_stage(E, t, g, C);
+            if (rc != CDSGD_OK) return rc;
+        }
+        if (!comp && E->p2p && E->pcorr) {
+            rc = p2p_reduce_async(E, t, C);
             if (rc != CDSGD_OK) return rc;
         }
         E->pending = true;

@@ -477,14 +477,15 @@ __global__ void __launch_bounds__(256) k_apply_quant(ApplyQArgs a, KeyTab kt, De
     int isq = 0;  // sum of cnt^2 on the table path: gsq += isq * (alpha/N)^2
     uint64_t bad_idx = NO_ERR;
     const bool do_loc = a.loc != nullptr;
-    constexpr int CLAIM = 2;
+    // small layouts (fewer than ~4 tiles per warp): claim single tiles for parallelism
+    const unsigned CLAIM = kt.ntiles < 4 * ((int64_t)gridDim.x * blockDim.x / 32) ? 1u : 2u;
     const bool dyn = a.sched != nullptr;
     int64_t cend = 0;
     if (dyn) {  // warps claim CLAIM tiles at a time from a global ticket (see k_fused_ldg)
         unsigned t0 = 0;
-        if (lane == 0) t0 = atomicAdd(a.sched, static_cast<unsigned>(CLAIM));
+        if (lane == 0) t0 = atomicAdd(a.sched, CLAIM);
         tb = __shfl_sync(FULL, t0, 0);
-        cend = tb + CLAIM < kt.ntiles ? tb + CLAIM : kt.ntiles;
+        cend = tb + (int64_t)CLAIM < kt.ntiles ? tb + (int64_t)CLAIM : kt.ntiles;
         te = tb < kt.ntiles ? kt.ntiles : tb;
     }
     if (tb < te && !skip) {
@@ -493,11 +494,11 @@ __global__ void __launch_bounds__(256) k_apply_quant(ApplyQArgs a, KeyTab kt, De
         for (int64_t ti = tb; ti < te; ++ti) {
             if (dyn && ti >= cend) {
                 unsigned t0 = 0;
-                if (lane == 0) t0 = atomicAdd(a.sched, static_cast<unsigned>(CLAIM));
+                if (lane == 0) t0 = atomicAdd(a.sched, CLAIM);
                 const int64_t nb = __shfl_sync(FULL, t0, 0);
                 if (nb >= kt.ntiles) break;
                 ti = nb;
-                cend = nb + CLAIM < kt.ntiles ? nb + CLAIM : kt.ntiles;
+                cend = nb + (int64_t)CLAIM < kt.ntiles ? nb + (int64_t)CLAIM : kt.ntiles;
             }
             kc.advance_to(kt, ti);
             const int64_t j = ti - kc.t0;

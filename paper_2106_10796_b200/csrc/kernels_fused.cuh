@@ -344,14 +344,15 @@ __global__ void __launch_bounds__(256, 2) k_fused_ldg(FusedArgs a, KeyTab kt, De
     int isq = 0;
     // Dynamic schedule: warps claim CLAIM consecutive tiles at a time from a global ticket,
     // so the kernel ends when the work does, not when the slowest static range does.
-    constexpr int CLAIM = 2;
+    // small layouts (fewer than ~4 tiles per warp): claim single tiles for parallelism
+    const unsigned CLAIM = kt.ntiles < 4 * ((int64_t)gridDim.x * blockDim.x / 32) ? 1u : 2u;
     const bool dyn = a.sched != nullptr;
     int64_t cbase = 0, cend = 0;
     if (dyn) {
         unsigned t0 = 0;
-        if (lane == 0) t0 = atomicAdd(a.sched, static_cast<unsigned>(CLAIM));
+        if (lane == 0) t0 = atomicAdd(a.sched, CLAIM);
         cbase = __shfl_sync(FULL, t0, 0);
-        cend = cbase + CLAIM < kt.ntiles ? cbase + CLAIM : kt.ntiles;
+        cend = cbase + (int64_t)CLAIM < kt.ntiles ? cbase + (int64_t)CLAIM : kt.ntiles;
         tb = cbase;
         te = cbase < kt.ntiles ? kt.ntiles : cbase;  // loop bound; real bound checked per claim
     }
@@ -362,11 +363,11 @@ __global__ void __launch_bounds__(256, 2) k_fused_ldg(FusedArgs a, KeyTab kt, De
             if (dyn) {
                 if (ti >= cend) {  // claim the next batch
                     unsigned t0 = 0;
-                    if (lane == 0) t0 = atomicAdd(a.sched, static_cast<unsigned>(CLAIM));
+                    if (lane == 0) t0 = atomicAdd(a.sched, CLAIM);
                     const int64_t nb = __shfl_sync(FULL, t0, 0);
                     if (nb >= kt.ntiles) break;
                     ti = nb;
-                    cend = nb + CLAIM < kt.ntiles ? nb + CLAIM : kt.ntiles;
+                    cend = nb + (int64_t)CLAIM < kt.ntiles ? nb + (int64_t)CLAIM : kt.ntiles;
                     if (ti < cc.t0) cc.seek(kt, ti);
                 }
             }
