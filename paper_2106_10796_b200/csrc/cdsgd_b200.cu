@@ -92,14 +92,7 @@ int flat_grid(K kernel, int64_t work) {
 }
 inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
-// TMA-staged kernels: one 256-thread CTA per SM, dynamic smem ring.
-bool use_ldg() {
-    static const bool v = [] {
-        const char* e = getenv("CDSGD_LDG");
-        return e != nullptr && e[0] == '1';
-    }();
-    return v;
-}
+// TMA-staged kernels (K1, K3): one CTA per SM, dynamic smem ring.
 template <typename K>
 bool prepare_tma(K kernel, int smem_bytes) {
     int d = 0;
@@ -262,32 +255,17 @@ extern "C" int cdsgd_quantize(const cdsgd_layout* L, const void* grad, int32_t g
     if (L->n == 0) return CDSGD_OK;
     if (!grad || !r_in || !r_out || !words) return fail(CDSGD_ERR_ARG, "NULL buffer");
     const KeyTab kt = L->tab();
-    if (!use_ldg()) {
-        int rc;
-        const P2PArgs nox{};
-        if (gdt == CDSGD_F32)
-            rc = launch_quant_tma_cfg(static_cast<const float*>(grad), r_in, r_out, words, kt, alpha, err, tag, S(stream),
-                                      nox);
-        else if (gdt == CDSGD_F64)
-            rc = launch_quant_tma_cfg(static_cast<const double*>(grad), r_in, r_out, words, kt, alpha, err, tag,
-                                      S(stream), nox);
-        else
-            return fail(CDSGD_ERR_ARG, "grad dtype must be CDSGD_F32 or CDSGD_F64");
-        if (rc != CDSGD_OK) return rc;
-        LAUNCH_CHECK();
-        return CDSGD_OK;
-    }
-    if (gdt == CDSGD_F32) {
-        const int grid = tile_grid(k_quantize<float>, kt.ntiles);
-        k_quantize<float><<<grid, THREADS, 0, S(stream)>>>(static_cast<const float*>(grad), r_in, r_out, words,
-                                                            kt, alpha, err, tag);
-    } else if (gdt == CDSGD_F64) {
-        const int grid = tile_grid(k_quantize<double>, kt.ntiles);
-        k_quantize<double><<<grid, THREADS, 0, S(stream)>>>(static_cast<const double*>(grad), r_in, r_out,
-                                                             words, kt, alpha, err, tag);
-    } else {
+    int rc;
+    const P2PArgs nox{};
+    if (gdt == CDSGD_F32)
+        rc = launch_quant_tma_cfg(static_cast<const float*>(grad), r_in, r_out, words, kt, alpha, err, tag, S(stream),
+                                  nox);
+    else if (gdt == CDSGD_F64)
+        rc = launch_quant_tma_cfg(static_cast<const double*>(grad), r_in, r_out, words, kt, alpha, err, tag,
+                                  S(stream), nox);
+    else
         return fail(CDSGD_ERR_ARG, "grad dtype must be CDSGD_F32 or CDSGD_F64");
-    }
+    if (rc != CDSGD_OK) return rc;
     LAUNCH_CHECK();
     return CDSGD_OK;
 }
@@ -474,53 +452,21 @@ int launch_apply_full(float* W, const float* gsum, int nr, int64_t n, double eta
     a.err = err;
     a.skip_below = skip_below;
     a.gnorm = gnorm;
-    if (!use_ldg()) {
-        const int rc = launch_af_tma_cfg(a, st);
-        if (rc != CDSGD_OK) return rc;
-        LAUNCH_CHECK();
-        return CDSGD_OK;
-    }
-    k_apply_full<<<flat_grid(k_apply_full, (n + 7) / 8), THREADS, 0, st>>>(a);
+    const int rc = launch_af_tma_cfg(a, st);
+    if (rc != CDSGD_OK) return rc;
     LAUNCH_CHECK();
     return CDSGD_OK;
 }
-// Fused apply(t-1) + quantize(t): LDG variant by default (measured faster than the TMA ring).
-int fused_cfg() {  // 0 (default) = register-staged LDG variant; <warps>x<stages> = TMA ring variant
-    static const int v = [] {
-        const char* e = getenv("CDSGD_FUSED_CFG");
-        if (e == nullptr || strcmp(e, "ldg") == 0) return 0;
-        return read_cfg("CDSGD_FUSED_CFG", 122);
-    }();
-    return v;
-}
-template <int NR, int AP, int WP, int ST>
-int launch_fused_t(const FusedArgs& a, const KeyTab& kt, const DecodeTab& tab, cudaStream_t st) {
-    using SM = FusedSmem<NR, AP, WP, ST>;
-    if constexpr (SM::BYTES > 227 * 1024) {
-        return launch_fused_t<NR, AP, 8, 2>(a, kt, tab, st);  // configuration does not fit: default
-    }
-    if (!prepare_tma(k_fused<NR, AP, WP, ST>, SM::BYTES)) return fail(CDSGD_ERR_CUDA, "smem attribute");
-    k_fused<NR, AP, WP, ST><<<tma_grid(kt.ntiles, WP), WP * 32, SM::BYTES, st>>>(a, kt, tab);
-    return CDSGD_OK;
-}
+// Fused apply(t-1) + quantize(t), register-staged (measured faster than a TMA-ring variant).
 template <int NR, int AP>
 int launch_fused_cfg(const FusedArgs& a, const KeyTab& kt, const DecodeTab& tab, cudaStream_t st) {
-    if (fused_cfg() == 0) {  // CDSGD_FUSED_CFG=ldg: register-staged variant, 2 CTAs/SM
-        k_fused_ldg<NR, AP><<<tile_grid(k_fused_ldg<NR, AP>, kt.ntiles), THREADS, 0, st>>>(a, kt, tab);
-        return CDSGD_OK;
-    }
-    switch (fused_cfg()) {
-        case 82: return launch_fused_t<NR, AP, 8, 2>(a, kt, tab, st);
-        case 62: return launch_fused_t<NR, AP, 6, 2>(a, kt, tab, st);
-        case 83: return launch_fused_t<NR, AP, 8, 3>(a, kt, tab, st);
-        default: return launch_fused_t<NR, AP, 12, 2>(a, kt, tab, st);
-    }
+    k_fused_ldg<NR, AP><<<tile_grid(k_fused_ldg<NR, AP>, kt.ntiles), THREADS, 0, st>>>(a, kt, tab);
+    return CDSGD_OK;
 }
 int launch_fused(int nr, int apply, const FusedArgs& a, const KeyTab& kt, const DecodeTab& tab, cudaStream_t st) {
     int rc;
     if (apply == APPLY_L) {  // W is final (P2P correction): only loc = W - eta_l*g and quantize
-        k_fused_ldg<1, APPLY_L><<<tile_grid(k_fused_ldg<1, APPLY_L>, kt.ntiles), THREADS, 0, st>>>(a, kt, tab);
-        rc = CDSGD_OK;
+        rc = launch_fused_cfg<1, APPLY_L>(a, kt, tab, st);
     } else if (apply == APPLY_F) {
         rc = launch_fused_cfg<1, APPLY_F>(a, kt, tab, st);
     } else {
@@ -899,7 +845,7 @@ extern "C" int cdsgd_engine_create(const cdsgd_engine_desc* d, const cdsgd_layou
     E->compute_is_loc = E->uses_local && E->n_warmup == 0;
     {
         const char* nf = getenv("CDSGD_NO_FUSE");
-        E->fuse = d->nranks == 1 && !(nf != nullptr && nf[0] == '1') && !use_ldg();
+        E->fuse = d->nranks == 1 && !(nf != nullptr && nf[0] == '1');
         const char* ns = getenv("CDSGD_STATIC_SCHED");
         if (!(ns != nullptr && ns[0] == '1')) {
             if (cudaMalloc(&E->sched, 4 * sizeof(unsigned int)) != cudaSuccess ||
@@ -964,7 +910,6 @@ extern "C" int cdsgd_engine_attach_p2p(cdsgd_engine* E, void* const* peer_bases,
     if (nranks != E->d.nranks || nranks < 2) return fail(CDSGD_ERR_ARG, "attach_p2p needs nranks == workers >= 2");
     if (nranks > MAX_RANKS_P2P) return fail(CDSGD_ERR_ARG, "fused exchange supports at most %d ranks", MAX_RANKS_P2P);
     if (E->t != 0) return fail(CDSGD_ERR_STATE, "attach_p2p must precede the first round");
-    if (use_ldg()) return fail(CDSGD_ERR_ARG, "fused exchange needs the TMA quantizer (unset CDSGD_LDG)");
     for (int r = 0; r < nranks; ++r) {
         if (peer_bases[r] == nullptr || (reinterpret_cast<uintptr_t>(peer_bases[r]) & 255) != 0)
             return fail(CDSGD_ERR_ARG, "peer base %d is NULL or not 256-byte aligned", r);

@@ -8,9 +8,9 @@
 //
 // Work unit: a "tile" = up to 32 packed words (512 elements) of ONE key. Tiles
 // never straddle keys (per-key packing restart, codec.py:147-148 via
-// engine.py:397-402), so only the last tile of a key can be partial. Each warp
-// owns a contiguous range of tiles (grid = resident warps), walks keys
-// incrementally and, for full 32B-aligned tiles, moves data with 128-bit
+// engine.py:397-402), so only the last tile of a key can be partial. Warps claim
+// tiles from a global ticket (or own a contiguous range), walk keys
+// incrementally and, for full 32B-aligned tiles, move data with 128-bit
 // (fp32) and 256-bit (fp64) vector loads/stores: lane l owns elements
 // [128c + 4l, 128c + 4l + 4) of chunk c (c = 0..3), so every warp-wide access
 // is fully coalesced. Codes are packed with two xor-shuffles (4 lanes -> one
@@ -65,22 +65,6 @@ __device__ __forceinline__ uint32_t ld_word(const uint32_t* p) {
     asm("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(v) : "l"(p));
     return v;
 }
-
-template <typename G> struct GVec;
-template <> struct GVec<float> {
-    float v[4];
-    __device__ __forceinline__ void load(const float* p) {
-        float4 t = ld_stream(p);
-        v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w;
-    }
-};
-template <> struct GVec<double> {
-    double v[4];
-    __device__ __forceinline__ void load(const double* p) {
-        d4 t = ld_stream(p);
-        v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w;
-    }
-};
 
 __device__ __forceinline__ bool aligned_to(const void* p, uintptr_t a) {
     return (reinterpret_cast<uintptr_t>(p) & (a - 1)) == 0;
@@ -286,95 +270,6 @@ __device__ __forceinline__ uint32_t quant1_lean(double r, G g, double alpha, uin
     return nz ? 1u + (ah >> 31) : 0u;
 }
 
-template <typename G>
-__global__ void __launch_bounds__(256) k_quantize(const G* __restrict__ g, const double* r_in,
-                                                  double* r_out, uint32_t* __restrict__ words,
-                                                  KeyTab kt, double alpha, uint64_t* err,
-                                                  uint64_t tag) {
-    if (err != nullptr && *reinterpret_cast<volatile uint64_t*>(err) != NO_ERR) return;
-    int64_t tb, te;
-    warp_range(kt.ntiles, tb, te);
-    if (tb >= te) return;
-    const int lane = threadIdx.x & 31;
-    TileCursor kc;
-    kc.seek(kt, tb);
-    uint64_t bad_idx = NO_ERR;
-    for (int64_t ti = tb; ti < te; ++ti) {
-        kc.advance_to(kt, ti);
-        const int64_t j = ti - kc.t0;
-        const int64_t e0 = kc.e0 + j * TILE_ELEMS;
-        const int64_t w0 = kc.w0 + j * TILE_WORDS;
-        const int64_t ne64 = kc.e1 - e0;
-        const int ne = ne64 < TILE_ELEMS ? static_cast<int>(ne64) : TILE_ELEMS;
-        const int64_t nw64 = kc.w1 - w0;
-        const int nw = nw64 < TILE_WORDS ? static_cast<int>(nw64) : TILE_WORDS;
-        const bool fast = ne == TILE_ELEMS && aligned_to(g + e0, 4 * sizeof(G)) &&
-                          aligned_to(r_in + e0, 32) && aligned_to(r_out + e0, 32);
-        uint32_t myword = 0;
-        if (fast) {
-            GVec<G> gv[CHUNKS];
-            d4 rv[CHUNKS];
-#pragma unroll
-            for (int c = 0; c < CHUNKS; ++c) {
-                const int64_t e = e0 + 128 * c + 4 * lane;
-                gv[c].load(g + e);
-                rv[c] = ld_stream(r_in + e);
-            }
-#pragma unroll
-            for (int c = 0; c < CHUNKS; ++c) {
-                const int64_t e = e0 + 128 * c + 4 * lane;
-                double o0, o1, o2, o3;
-                bool b0, b1, b2, b3;
-                uint32_t code = quant1(rv[c].x, gv[c].v[0], alpha, o0, b0);
-                code |= quant1(rv[c].y, gv[c].v[1], alpha, o1, b1) << 2;
-                code |= quant1(rv[c].z, gv[c].v[2], alpha, o2, b2) << 4;
-                code |= quant1(rv[c].w, gv[c].v[3], alpha, o3, b3) << 6;
-                st_stream(r_out + e, o0, o1, o2, o3);
-                if (b0 | b1 | b2 | b3) {
-                    const int first = b0 ? 0 : b1 ? 1 : b2 ? 2 : 3;
-                    const uint64_t idx = tag | static_cast<uint64_t>(e + first);
-                    bad_idx = idx < bad_idx ? idx : bad_idx;
-                }
-                // 4 lanes x 8 bits -> word (8c + lane/4) of this tile
-                uint32_t v = code << (8 * (lane & 3));
-                v |= __shfl_xor_sync(FULL, v, 1);
-                v |= __shfl_xor_sync(FULL, v, 2);
-                const uint32_t s = __shfl_sync(FULL, v, 4 * (lane & 7));
-                if ((lane >> 3) == c) myword = s;
-            }
-        } else {
-#pragma unroll 4
-            for (int s = 0; s < TILE_ELEMS / 32; ++s) {
-                const int el = 32 * s + lane;
-                const bool valid = el < ne;
-                bool p = false, m = false;
-                if (valid) {
-                    double o;
-                    bool b;
-                    const uint32_t code = quant1(r_in[e0 + el], g[e0 + el], alpha, o, b);
-                    r_out[e0 + el] = o;
-                    p = code == 1u;
-                    m = code == 2u;
-                    if (b) {
-                        const uint64_t idx = tag | static_cast<uint64_t>(e0 + el);
-                        bad_idx = idx < bad_idx ? idx : bad_idx;
-                    }
-                }
-                const uint32_t pm = __ballot_sync(FULL, p);
-                const uint32_t mm = __ballot_sync(FULL, m);
-                if (lane == 2 * s) myword = interleave_codes(pm, mm);
-                if (lane == 2 * s + 1) myword = interleave_codes(pm >> 16, mm >> 16);
-            }
-        }
-        if (lane < nw) words[w0 + lane] = myword;
-    }
-    if (err != nullptr) {
-        bad_idx = warp_min_u64(bad_idx);
-        if (lane == 0 && bad_idx != NO_ERR) atomicMin(reinterpret_cast<unsigned long long*>(err),
-                                                      static_cast<unsigned long long>(bad_idx));
-    }
-}
-
 // ================================================================ decode helpers
 // Exact-alpha mode (the usual alpha = 0.5): every partial sum j*alpha, |j| <= N,
 // is representable, so the ascending-worker fp64 sum of engine.py:250-253 equals
@@ -401,13 +296,6 @@ __device__ __forceinline__ void count_add(Counts& c, uint32_t w) {
     c.po += (w >> 2) & 0x11111111u;
     c.mo += (w >> 3) & 0x11111111u;
     c.rsv |= w & (w >> 1) & 0x55555555u;
-}
-// signed count for code position j (0..15)
-__device__ __forceinline__ int count_at(const Counts& c, int j) {
-    const int sh = 4 * (j >> 1);
-    const uint32_t p = (j & 1) ? c.po : c.pe;
-    const uint32_t m = (j & 1) ? c.mo : c.me;
-    return static_cast<int>((p >> sh) & 15u) - static_cast<int>((m >> sh) & 15u);
 }
 // Signed counts of this lane's 4 code positions 4*(lane&3) .. +3 in one word:
 // shift the SWAR counters once, then extract fields with constant shifts.
@@ -712,80 +600,6 @@ struct ApplyFArgs {
     uint64_t skip_below;
     double* gnorm;
 };
-
-__global__ void __launch_bounds__(256) k_apply_full(ApplyFArgs a) {
-    if (a.err != nullptr && *reinterpret_cast<volatile const uint64_t*>(a.err) < a.skip_below) return;
-    const bool do_loc = a.loc != nullptr;
-    const bool vec = aligned_to(a.W, 16) && aligned_to(a.gsum, 16) &&
-                     (!do_loc || (aligned_to(a.gnext, 16) && aligned_to(a.loc, 16)));
-    const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    const int64_t nth = (int64_t)gridDim.x * blockDim.x;
-    double gsq = 0.0;
-    int64_t done = 0;
-    if (vec) {
-        const int64_t nv = a.n / 4;
-        constexpr int U = 2;
-        int64_t i = tid;
-        for (; i + (U - 1) * nth < nv; i += U * nth) {
-            float4 w[U], s[U], g[U];
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-                w[u] = ld_stream(a.W + 4 * (i + u * nth));
-                s[u] = ld_stream(a.gsum + 4 * (i + u * nth));
-                if (do_loc) g[u] = ld_stream(a.gnext + 4 * (i + u * nth));
-            }
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-                float4 o;
-                o.x = __fmaf_rn(-a.scale, s[u].x, w[u].x);
-                o.y = __fmaf_rn(-a.scale, s[u].y, w[u].y);
-                o.z = __fmaf_rn(-a.scale, s[u].z, w[u].z);
-                o.w = __fmaf_rn(-a.scale, s[u].w, w[u].w);
-                st_stream(a.W + 4 * (i + u * nth), o.x, o.y, o.z, o.w);
-                if (do_loc)
-                    st_stream(a.loc + 4 * (i + u * nth), __fmaf_rn(-a.eta_l, g[u].x, o.x),
-                              __fmaf_rn(-a.eta_l, g[u].y, o.y), __fmaf_rn(-a.eta_l, g[u].z, o.z),
-                              __fmaf_rn(-a.eta_l, g[u].w, o.w));
-                if (a.gnorm != nullptr) {
-                    const double m0 = s[u].x * a.inv_n, m1 = s[u].y * a.inv_n, m2 = s[u].z * a.inv_n,
-                                 m3 = s[u].w * a.inv_n;
-                    gsq += m0 * m0 + m1 * m1 + m2 * m2 + m3 * m3;
-                }
-            }
-        }
-        for (; i < nv; i += nth) {
-            float4 w = ld_stream(a.W + 4 * i), s = ld_stream(a.gsum + 4 * i);
-            float4 o;
-            o.x = __fmaf_rn(-a.scale, s.x, w.x);
-            o.y = __fmaf_rn(-a.scale, s.y, w.y);
-            o.z = __fmaf_rn(-a.scale, s.z, w.z);
-            o.w = __fmaf_rn(-a.scale, s.w, w.w);
-            st_stream(a.W + 4 * i, o.x, o.y, o.z, o.w);
-            if (do_loc) {
-                float4 g = ld_stream(a.gnext + 4 * i);
-                st_stream(a.loc + 4 * i, __fmaf_rn(-a.eta_l, g.x, o.x), __fmaf_rn(-a.eta_l, g.y, o.y),
-                          __fmaf_rn(-a.eta_l, g.z, o.z), __fmaf_rn(-a.eta_l, g.w, o.w));
-            }
-            if (a.gnorm != nullptr) {
-                const double m0 = s.x * a.inv_n, m1 = s.y * a.inv_n, m2 = s.z * a.inv_n, m3 = s.w * a.inv_n;
-                gsq += m0 * m0 + m1 * m1 + m2 * m2 + m3 * m3;
-            }
-        }
-        done = nv * 4;
-    }
-    for (int64_t i = done + tid; i < a.n; i += nth) {
-        const float s = a.gsum[i];
-        const float wn = __fmaf_rn(-a.scale, s, a.W[i]);
-        a.W[i] = wn;
-        if (do_loc) a.loc[i] = __fmaf_rn(-a.eta_l, a.gnext[i], wn);
-        if (a.gnorm != nullptr) { const double m = s * a.inv_n; gsq += m * m; }
-    }
-    if (a.gnorm != nullptr) {
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) gsq += __shfl_xor_sync(FULL, gsq, o);
-        if ((threadIdx.x & 31) == 0 && gsq != 0.0) atomicAdd(a.gnorm, gsq);
-    }
-}
 
 // engine.global_update / local_update with fp64 math (exact reference arithmetic
 // for fp64 operands; one rounding to the output type otherwise).

@@ -9,12 +9,12 @@
 //   writes r' 8 | codes(t) 1/4 | W 4 | loc 4
 //   = 32 + (N+1)/4 B/elem (APPLY_Q) vs 36.5 + N/4 for K1 + K2 separately.
 //
-// Staging as in kernels_tma.cuh: per-warp smem ring filled by cp.async.bulk, one
-// CTA per SM. With the fused P2P exchange the kernel both waits for the peers'
-// codes of round t-1 and for the release of the slot round t writes into, and its
-// last CTA publishes ready(t) and freed(t-1).
+// With the fused P2P exchange the kernel both waits for the peers' codes of round t-1
+// and for the release of the slot round t writes into, and its last CTA publishes
+// ready(t) and freed(t-1). (A TMA-ring variant of this kernel was measured ~3 %
+// slower at ResNet-50 size and removed.)
 #pragma once
-#include "kernels_tma.cuh"
+#include "kernels.cuh"
 
 namespace cdsgd {
 
@@ -45,286 +45,8 @@ struct FusedArgs {
     unsigned int* sched;  // [2] dynamic tile scheduler {next tile, CTAs done}; nullptr = static ranges
 };
 
-template <int NR, int APPLY, int WARPS, int S>
-struct FusedSmem {
-    static constexpr int G = TILE_ELEMS * 4, R = TILE_ELEMS * 8, WB = TILE_ELEMS * 4;
-    static constexpr int X = APPLY == APPLY_F ? TILE_ELEMS * 4 : NR * CODE_WIN;
-    static constexpr int SLOT = G + R + WB + X;
-    static constexpr int WARP = S * SLOT;
-    static constexpr int BYTES = WARPS * WARP + WARPS * S * 8;
-};
-
-template <int NR, int APPLY, int WARPS, int S>
-__global__ void __launch_bounds__(WARPS * 32, 1) k_fused(FusedArgs a, KeyTab kt, DecodeTab tab) {
-    using SM = FusedSmem<NR, APPLY, WARPS, S>;
-    extern __shared__ __align__(128) unsigned char smem[];
-    __shared__ float s_upd[2 * MAX_RANKS + 1];
-    p2p_wait2(a.xq, a.xa);
-    const uint64_t e0v = a.err != nullptr ? *reinterpret_cast<volatile uint64_t*>(a.err) : ~0ull;
-    const bool q_off = e0v != NO_ERR;        // sticky abort of quantization
-    const bool a_off = e0v < a.skip_below;   // an error in round <= t-1: do not apply it
-    if (APPLY == APPLY_Q && threadIdx.x < 2 * NR + 1) s_upd[threadIdx.x] = tab.upd[threadIdx.x];
-    __syncthreads();
-    const int warp = threadIdx.x >> 5;
-    const int lane = threadIdx.x & 31;
-    unsigned char* ring = smem + warp * SM::WARP;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + WARPS * SM::WARP) + warp * S;
-    const char* gbase = reinterpret_cast<const char*>(a.gathered);
-    const char* gend = gbase + 4 * (NR * a.stride);
-    const uint32_t ahi = static_cast<uint32_t>(__double2hiint(a.alpha));
-    const uint32_t alo = static_cast<uint32_t>(__double2loint(a.alpha));
-    int64_t tb, te;
-    warp_range(kt.ntiles, tb, te);
-    uint64_t bad_idx = NO_ERR, bad_sym = NO_ERR;
-    double gsq = 0.0;
-    int isq = 0;  // sum of cnt^2 (APPLY_Q): gsq += isq * (alpha/N)^2
-    if (tb < te) {
-        if (lane == 0) {
-            for (int s = 0; s < S; ++s) tma::mbar_init(&bars[s], 1);
-            tma::fence_mbar_init();
-        }
-        __syncwarp();
-        TileCursor pc, cc;
-        pc.seek(kt, tb);
-        cc = pc;
-        uint32_t staged = 0, phase = 0;
-        auto issue = [&](int64_t ti, int slot) {
-            pc.advance_to(kt, ti);
-            const int64_t jj = ti - pc.t0;
-            const int64_t e0 = pc.e0 + jj * TILE_ELEMS;
-            const int64_t w0 = pc.w0 + jj * TILE_WORDS;
-            bool ok = pc.e1 - e0 >= TILE_ELEMS && aligned_to(a.g + e0, 16) && aligned_to(a.r_in + e0, 16) &&
-                      aligned_to(a.r_out + e0, 32) && aligned_to(a.W + e0, 16) && aligned_to(a.loc + e0, 16);
-            uint32_t bytes = SM::G + SM::R + SM::WB;
-            const char* lo[APPLY == APPLY_Q ? NR : 1];
-            uint32_t len[APPLY == APPLY_Q ? NR : 1];
-            if constexpr (APPLY == APPLY_Q) {
-#pragma unroll
-                for (int r = 0; r < NR; ++r) {
-                    const char* src = reinterpret_cast<const char*>(a.gathered + r * a.stride + w0);
-                    lo[r] = reinterpret_cast<const char*>(reinterpret_cast<uintptr_t>(src) & ~uintptr_t(15));
-                    const char* hi = reinterpret_cast<const char*>(
-                        (reinterpret_cast<uintptr_t>(src) + 4 * TILE_WORDS + 15) & ~uintptr_t(15));
-                    len[r] = static_cast<uint32_t>(hi - lo[r]);
-                    ok = ok && lo[r] >= gbase && hi <= gend;
-                    bytes += len[r];
-                }
-            } else {
-                ok = ok && aligned_to(a.gsum + e0, 16);
-                bytes += SM::X;
-            }
-            if (ok) {
-                if (lane == 0) {
-                    unsigned char* sl = ring + slot * SM::SLOT;
-                    tma::arrive_expect_tx(&bars[slot], bytes);
-                    tma::bulk_g2s(sl, a.g + e0, SM::G, &bars[slot]);
-                    tma::bulk_g2s(sl + SM::G, a.r_in + e0, SM::R, &bars[slot]);
-                    tma::bulk_g2s(sl + SM::G + SM::R, a.W + e0, SM::WB, &bars[slot]);
-                    unsigned char* sx = sl + SM::G + SM::R + SM::WB;
-                    if constexpr (APPLY == APPLY_Q) {
-#pragma unroll
-                        for (int r = 0; r < NR; ++r) tma::bulk_g2s(sx + r * CODE_WIN, lo[r], len[r], &bars[slot]);
-                    } else {
-                        tma::bulk_g2s(sx, a.gsum + e0, SM::X, &bars[slot]);
-                    }
-                }
-                staged |= 1u << slot;
-            } else {
-                staged &= ~(1u << slot);
-            }
-        };
-        for (int i = 0; i < S - 1 && tb + i < te; ++i) issue(tb + i, i);
-        int slot = 0;
-        for (int64_t ti = tb; ti < te; ++ti) {
-            if (ti + S - 1 < te) {
-                __syncwarp();  // slot being refilled was fully read last iteration (WAR, no proxy fence)
-                issue(ti + S - 1, slot == 0 ? S - 1 : slot - 1);
-            }
-            cc.advance_to(kt, ti);
-            const int64_t j = ti - cc.t0;
-            const int64_t e0 = cc.e0 + j * TILE_ELEMS;
-            const int64_t w0 = cc.w0 + j * TILE_WORDS;
-            const int64_t ne64 = cc.e1 - e0;
-            const int ne = ne64 < TILE_ELEMS ? static_cast<int>(ne64) : TILE_ELEMS;
-            const int64_t nw64 = cc.w1 - w0;
-            const int nw = nw64 < TILE_WORDS ? static_cast<int>(nw64) : TILE_WORDS;
-            uint32_t myword = 0;
-            if (staged & (1u << slot)) {
-                tma::wait(&bars[slot], (phase >> slot) & 1u);
-                phase ^= 1u << slot;
-                const unsigned char* sl = ring + slot * SM::SLOT;
-                const float* sg = reinterpret_cast<const float*>(sl);
-                const double* sr = reinterpret_cast<const double*>(sl + SM::G);
-                const float* sW = reinterpret_cast<const float*>(sl + SM::G + SM::R);
-                const unsigned char* sx = sl + SM::G + SM::R + SM::WB;
-                uint32_t off[APPLY == APPLY_Q ? NR : 1];
-                if constexpr (APPLY == APPLY_Q) {
-#pragma unroll
-                    for (int r = 0; r < NR; ++r)
-                        off[r] = static_cast<uint32_t>(reinterpret_cast<uintptr_t>(a.gathered + r * a.stride + w0) & 15u);
-                }
-                uint32_t v[CHUNKS];
-                bool bad = false;
-                const int jb = 4 * (lane & 3);
-#pragma unroll
-                for (int c = 0; c < CHUNKS; ++c) {
-                    float gv[4], wv[4];
-                    double rv[4];
-                    tma::lds4(sg + 128 * c, lane, gv);
-                    tma::lds4(sr + 128 * c, lane, rv);
-                    tma::lds4(sW + 128 * c, lane, wv);
-                    const int64_t e = e0 + 128 * c + 4 * lane;
-                    // ---- apply(t-1): W_t and loc_{t+1} = W_t - eta_l * g_t
-                    if (!a_off) {
-                        float l4[4];
-                        if constexpr (APPLY == APPLY_Q) {
-                            Counts cnt{0u, 0u, 0u, 0u, 0u};
-                            const int widx = 8 * c + (lane >> 2);
-#pragma unroll
-                            for (int r = 0; r < NR; ++r)
-                                count_add(cnt, *reinterpret_cast<const uint32_t*>(sx + r * CODE_WIN + off[r] + 4 * widx));
-                            int cq[4];
-                            lane_counts(cnt, lane, cq);
-#pragma unroll
-                            for (int q = 0; q < 4; ++q) {
-                                wv[q] = __fsub_rn(wv[q], s_upd[cq[q] + NR]);
-                                l4[q] = __fmaf_rn(-a.eta_l, gv[q], wv[q]);
-                                isq += cq[q] * cq[q];
-                            }
-                            if (((cnt.rsv >> (2 * jb)) & 0xffu) != 0u) {
-                                const int q = __ffs((cnt.rsv >> (2 * jb)) & 0x55u) / 2;
-                                bad_sym = static_cast<uint64_t>(e + q) < bad_sym ? static_cast<uint64_t>(e + q) : bad_sym;
-                            }
-                        } else {
-                            float s4[4];
-                            tma::lds4(reinterpret_cast<const float*>(sx) + 128 * c, lane, s4);
-#pragma unroll
-                            for (int q = 0; q < 4; ++q) {
-                                wv[q] = __fmaf_rn(-a.scale, s4[q], wv[q]);
-                                l4[q] = __fmaf_rn(-a.eta_l, gv[q], wv[q]);
-                                if (a.gnorm != nullptr) {
-                                    const double m = s4[q] * a.inv_n;
-                                    gsq = __fma_rn(m, m, gsq);
-                                }
-                            }
-                        }
-                        st_stream(a.W + e, wv[0], wv[1], wv[2], wv[3]);
-                        st_stream(a.loc + e, l4[0], l4[1], l4[2], l4[3]);
-                    }
-                    // ---- quantize(t)
-                    if (!q_off) {
-                        double o[4];
-                        uint32_t code = 0;
-#pragma unroll
-                        for (int q = 0; q < 4; ++q)
-                            code |= quant1_lean(rv[q], gv[q], a.alpha, ahi, alo, o[q], bad) << (2 * q);
-                        st_stream(a.r_out + e, o[0], o[1], o[2], o[3]);
-                        v[c] = code << (8 * (lane & 3));
-                    } else {
-                        v[c] = 0;
-                    }
-                }
-                if (__any_sync(FULL, bad))
-                    bad_idx = rescan_nonfinite(sg, sr, lane, e0, a.tag, bad_idx);
-#pragma unroll
-                for (int c = 0; c < CHUNKS; ++c) v[c] |= __shfl_xor_sync(FULL, v[c], 1);
-#pragma unroll
-                for (int c = 0; c < CHUNKS; ++c) v[c] |= __shfl_xor_sync(FULL, v[c], 2);
-#pragma unroll
-                for (int c = 0; c < CHUNKS; ++c) {
-                    const uint32_t w = __shfl_sync(FULL, v[c], 4 * (lane & 7));
-                    if ((lane >> 3) == c) myword = w;
-                }
-            } else {
-                // partial / misaligned tile: coalesced scalar path, lane l owns element 32s + l
-                uint32_t cw[APPLY == APPLY_Q ? NR : 1];
-                if constexpr (APPLY == APPLY_Q) {
-#pragma unroll
-                    for (int r = 0; r < NR; ++r) cw[r] = lane < nw ? a.gathered[r * a.stride + w0 + lane] : 0u;
-                }
-#pragma unroll 2
-                for (int s = 0; s < TILE_ELEMS / 32; ++s) {
-                    const int el = 32 * s + lane;
-                    int cn = 0;
-                    bool rsv = false;
-                    if constexpr (APPLY == APPLY_Q) {
-#pragma unroll
-                        for (int r = 0; r < NR; ++r) {
-                            const uint32_t cd = (__shfl_sync(FULL, cw[r], 2 * s + (lane >> 4)) >> (2 * (lane & 15))) & 3u;
-                            rsv |= cd == 3u;
-                            cn += (cd == 1u) - (cd == 2u);
-                        }
-                    }
-                    bool p = false, m = false;
-                    if (el < ne) {
-                        const int64_t e = e0 + el;
-                        const float gval = a.g[e];
-                        if (!a_off) {
-                            float wn;
-                            if constexpr (APPLY == APPLY_Q) {
-                                wn = __fsub_rn(a.W[e], s_upd[cn + NR]);
-                                isq += cn * cn;
-                                if (rsv) bad_sym = static_cast<uint64_t>(e) < bad_sym ? static_cast<uint64_t>(e) : bad_sym;
-                            } else {
-                                const float sv = a.gsum[e];
-                                wn = __fmaf_rn(-a.scale, sv, a.W[e]);
-                                if (a.gnorm != nullptr) { const double mm = sv * a.inv_n; gsq = __fma_rn(mm, mm, gsq); }
-                            }
-                            a.W[e] = wn;
-                            a.loc[e] = __fmaf_rn(-a.eta_l, gval, wn);
-                        }
-                        if (!q_off) {
-                            double o;
-                            bool b;
-                            const uint32_t code = quant1(a.r_in[e], gval, a.alpha, o, b);
-                            a.r_out[e] = o;
-                            p = code == 1u;
-                            m = code == 2u;
-                            if (b) {
-                                const uint64_t idx = a.tag | static_cast<uint64_t>(e);
-                                bad_idx = idx < bad_idx ? idx : bad_idx;
-                            }
-                        }
-                    }
-                    const uint32_t pm = __ballot_sync(FULL, p);
-                    const uint32_t mm = __ballot_sync(FULL, m);
-                    if (lane == 2 * s) myword = interleave_codes(pm, mm);
-                    if (lane == 2 * s + 1) myword = interleave_codes(pm >> 16, mm >> 16);
-                }
-            }
-            if (lane < nw && !q_off) {
-                if (a.xq.nranks > 0) {
-                    for (int r = 0; r < a.xq.nranks; ++r) a.xq.dst[r][w0 + lane] = myword;
-                } else {
-                    a.words[w0 + lane] = myword;
-                }
-            }
-            slot = slot + 1 == S ? 0 : slot + 1;
-        }
-    }
-    if (a.gnorm != nullptr) {
-        gsq += static_cast<double>(isq) * tab.sq_scale;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) gsq += __shfl_xor_sync(FULL, gsq, o);
-        if (lane == 0 && gsq != 0.0) atomicAdd(a.gnorm, gsq);
-    }
-    if (a.err != nullptr) {
-        bad_idx = warp_min_u64(bad_idx);
-        bad_sym = warp_min_u64(bad_sym);
-        if (lane == 0 && bad_idx != NO_ERR)
-            atomicMin(reinterpret_cast<unsigned long long*>(a.err), static_cast<unsigned long long>(bad_idx));
-        if (lane == 0 && bad_sym != NO_ERR)
-            atomicMin(reinterpret_cast<unsigned long long*>(a.err + 1), static_cast<unsigned long long>(bad_sym));
-    }
-    p2p_publish2(a.xq, a.xa, a.xq.counter != nullptr ? a.xq.counter : a.xa.counter);
-}
-
-}  // namespace cdsgd
-
-namespace cdsgd {
-// LDG variant of k_fused: same arithmetic and protocol, data moved with 128/256-bit
-// coalesced loads straight into registers (all loads of a tile issued first), two
-// 256-thread CTAs per SM instead of the TMA ring.
+// Data moved with 128/256-bit coalesced loads straight into registers (all loads of a
+// tile issued first), two 256-thread CTAs per SM, dynamic tile scheduling.
 template <int NR, int APPLY>
 __global__ void __launch_bounds__(256, 2) k_fused_ldg(FusedArgs a, KeyTab kt, DecodeTab tab) {
     __shared__ float s_upd[2 * MAX_RANKS + 1];

@@ -240,10 +240,6 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
     p2p_publish(x);
 }
 
-// Code window per rank staged by the fused TMA kernel: a 16-byte-aligned window
-// (<= 144 B) around a tile's 32 code words.
-constexpr int CODE_WIN = 144;
-
 // ================================================================ K3 (TMA)
 template <int WARPS, int S>
 struct ApplyFSmem {
