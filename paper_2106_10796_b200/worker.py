@@ -141,8 +141,11 @@ class CDSGDWorker:
             raise ConfigError("symmetric memory group does not match hp.workers")
         arr = (C.c_void_p * self.world)(*ptrs)
         _lib.check(lib.cdsgd_engine_attach_p2p(self._eng, arr, self.world, int(exact)), "cdsgd_engine_attach_p2p")
-        # the engine moved the W replica into the symmetric buffer (peers write W' shards into it)
+        # the engine moved the W replica into the symmetric buffer (peers write W' shards into it),
+        # and the code slots live there too (slot 0 at offset 0, slot 1 at the next 256-B boundary)
         self.W = self._symm[w_off:w_off + 4 * n].view(torch.float32)
+        slot = (self.world * nw * 4 + 255) // 256 * 256
+        self.gathered = [self._symm[i * slot:i * slot + self.world * nw * 4].view(torch.uint32) for i in range(2)]
         torch.cuda.synchronize(self.device)
         dist.barrier(group=grp)  # every rank's flags are zero before any rank's first K1
 
@@ -175,6 +178,25 @@ class CDSGDWorker:
         if r < 0:
             raise ConfigError(_lib.last_error())
         return bool(r)
+
+    def round_payloads(self, t: int) -> list:
+        """This rank's per-key QuantizedPayloads of compressed round t (engine.py:397-402),
+        as views of the packed code buffer — valid until round t+2 reuses the slot. Feed them
+        to ``wire.round_frames`` to talk to the reference ServerNode."""
+        from .codec import QuantizedPayload
+
+        if not (0 <= t < self.t) or t < self.t - 2:
+            raise ConfigError(f"round {t} is not among the last two started rounds")
+        if not self.round_compressed(t):
+            raise ConfigError(f"round {t} pushed full-precision gradients, not codes")
+        nw = self.layout.n_words
+        mine = self.gathered[t % 2][self.rank * nw:(self.rank + 1) * nw]
+        out, w0 = [], 0
+        for span in self.layout.spans:
+            k = (span.length + 15) // 16
+            out.append(QuantizedPayload(mine[w0:w0 + k], self.hp.alpha, span.length))
+            w0 += k
+        return out
 
     def grad_norm(self, t: int) -> float:
         """||round-t mean gradient||_2 (engine.py:521); valid for the last gnorm_ring rounds."""

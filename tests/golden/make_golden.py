@@ -207,8 +207,30 @@ ENGINE_CASES = [
 ]
 
 
+def wire_cases():
+    """Frames of every variant from the reference encoder (protocol.py:116-140)."""
+    import cdsgd.protocol as protocol
+
+    rng = np.random.default_rng(77)
+    g = (0.6 * rng.standard_normal(37)).astype(np.float32)
+    payload, _ = codec.quantize(codec.ResidualState.zeros(37), g, 0.5)
+    vals = rng.standard_normal(5)
+    msgs = {
+        "push_quant": protocol.PushQuantized(3, 123456789, 7, payload),
+        "push_full": protocol.PushFull(2, 41, 1, vals),
+        "pull": protocol.PullRequest(5, 9),
+        "weights": protocol.Weights(12, 3, vals),
+        "shutdown": protocol.Shutdown(),
+    }
+    out = {"wire_grad": g, "wire_vals": vals}
+    for name, m in msgs.items():
+        out[f"wire_{name}"] = np.frombuffer(protocol.encode_message(m), dtype=np.uint8)
+    return out
+
+
 def main():
     codec_out = codec_cases()
+    codec_out.update(wire_cases())
     np.savez_compressed(os.path.join(HERE, "codec_golden.npz"), **codec_out)
     eng = {}
     names = []

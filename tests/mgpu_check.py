@@ -59,6 +59,9 @@ def run_case(case, exchange, comm, rank, world, dev):
         res = wk.residual.cpu().numpy()
         assert np.array_equal(res.view(np.uint64), orc.workers[rank].residual.view(np.uint64)), \
             f"{tag} residual round {t}"
+        if orc.compressed[t]:  # this rank's codes of the round, as the engine exposes them
+            got = np.concatenate([p.words.cpu().numpy() for p in wk.round_payloads(t)])
+            assert np.array_equal(got, orc.words[(t, rank)]), f"{tag} codes round {t}"
     wk.flush()
     W = wk.weights
     np.testing.assert_allclose(W.cpu().numpy(), orc.W, rtol=RTOL, atol=ATOL, err_msg=f"{tag} W")

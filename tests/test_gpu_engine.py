@@ -213,3 +213,29 @@ def test_apply_quant_fused_local_update(pkg):
     _lib.check(lib.cdsgd_apply_quant(layout.handle().ptr, Wd.data_ptr(), words.data_ptr(), 1, layout.n_words, 0.5, 0.1,
                                      None, None, 0.4, err.data_ptr(), 0, None, torch.cuda.current_stream().cuda_stream))
     assert int(err[1].item()) == 16 * 3 + 5
+
+
+def test_round_payloads_to_reference_frames(pkg):
+    """The engine's codes of a round, framed for the reference PS (wire.py), carry the
+    oracle's words bit for bit."""
+    from paper_2106_10796_b200 import wire
+
+    _, E, L, Wk = pkg
+    sizes = [1000, 37, 16, 1]
+    layout = L.Layout.from_lengths(sizes)
+    hp = E.HyperParams(algo="cdsgd", workers=1, k=4, warmup_n=0)
+    w0 = O.synthetic_weights(6, layout.total)
+    wk = Wk.CDSGDWorker(layout, hp, w0)
+    orc = O.LockstepOracle(w0.astype(np.float64), sizes, O.OracleHP("cdsgd", 1, 0.1, None, 4, 0.5, 0))
+    for t in range(6):
+        g = O.synthetic_grad(6, t, 0, layout.total)
+        wk.step(torch.from_numpy(g).cuda())
+        orc.step([g])
+        if orc.compressed[t]:
+            frames = wire.round_frames(0, t, payloads=wk.round_payloads(t))
+            assert len(frames) == len(sizes)
+            got = np.concatenate([wire.decode_frame(f).payload.words.cpu().numpy() for f in frames])
+            assert np.array_equal(got, orc.words[(t, 0)]), t
+        else:
+            with pytest.raises(E.ConfigError):
+                wk.round_payloads(t)
