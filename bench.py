@@ -306,15 +306,22 @@ def run_ours(args):
             "frac": kernels[dom]["achieved_gbs"] / peak, "traffic": ncu_traffic(args.workload, dom),
             "algorithmic_bytes_per_launch": alg[dom], "peak_source": peak_src}
     exch = None
-    if world > 1 and prof["exchange"]["n"]:
+    if world > 1:
         P = 4 * nw
         n_comp = sum(1 for i in range(K) if wk.round_compressed(W + i))
         n_full = K - n_comp
-        bus_bytes = n_comp * (world - 1) * P + n_full * 2 * (world - 1) / world * 4 * n
-        exch = {"calls": prof["exchange"]["n"], "total_ms": prof["exchange"]["ms"],
-                "bus_gbs": bus_bytes / (prof["exchange"]["ms"] / 1e3) / 1e9, "nvlink_peak_gbs": 900.0,
-                "allgather_bytes_per_rank": P, "allreduce_bytes": 4 * n}
-        exch["bus_frac"] = exch["bus_gbs"] / 900.0
+        nccl_codes = args.exchange == "nccl"
+        exch = {"mode": args.exchange, "code_bytes_per_rank_per_round": P,
+                "code_bus_bytes_per_round": (world - 1) * P,
+                "code_path": "ncclAllGather" if nccl_codes else "NVLink stores inside the quantizing kernel",
+                "correction_bytes": 4 * n,
+                "correction_path": "sharded fp64 NVLink reduce" if args.exchange == "p2p-exact" else "ncclAllReduce"}
+        if prof["exchange"]["n"]:
+            # NCCL calls on the exchange stream: all-gathers (nccl mode) and correction all-reduces
+            bus_bytes = (n_comp * (world - 1) * P if nccl_codes else 0) + n_full * 2 * (world - 1) / world * 4 * n
+            exch.update({"nccl_calls": prof["exchange"]["n"], "nccl_total_ms": prof["exchange"]["ms"],
+                         "nccl_bus_gbs": bus_bytes / (prof["exchange"]["ms"] / 1e3) / 1e9, "nvlink_peak_gbs": 900.0})
+            exch["nccl_bus_frac"] = exch["nccl_bus_gbs"] / 900.0
 
     # ---------------- end-to-end through the public API with host buffers
     e2e = None

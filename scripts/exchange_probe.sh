@@ -11,7 +11,7 @@ l=[x for x in open(f"gpurun_out/xp_{sys.argv[1]}_{sys.argv[2]}.log") if x.starts
 if not l: print(sys.argv[1:], open(f"gpurun_out/xp_{sys.argv[1]}_{sys.argv[2]}.log").read()[-1500:]); sys.exit()
 d=json.loads(l[-1]); ks=" ".join(f"{k}={v['avg_us']:.0f}" for k,v in d["kernels"].items())
 x=d.get("exchange") or {}
-print(f"{sys.argv[1]:5s} k={sys.argv[2]:5s} value={d['value']:.1f} step={d['ms_per_step']*1e3:.1f}us  {ks}  xcalls={x.get('calls')} x_us={x and x['total_ms']*1e3/max(1,x['calls']):.0f}")
+print(f"{sys.argv[1]:5s} k={sys.argv[2]:5s} value={d['value']:.1f} step={d['ms_per_step']*1e3:.1f}us  {ks}  xcalls={x.get('calls')} x_us={x and x['nccl_total_ms']*1e3/max(1,x['nccl_calls']):.0f}")
 PY
   done
 done

@@ -12,7 +12,7 @@ f=f"gpurun_out/mes_{sys.argv[1]}.log"
 l=[x for x in open(f) if x.startswith("{")]
 if not l: print(sys.argv[2], open(f).read()[-1500:]); sys.exit()
 d=json.loads(l[-1]); ks=" ".join(f"{k}={v['avg_us']:.0f}" for k,v in d["kernels"].items())
-x=d['exchange']
-print(f"{sys.argv[2]:45s} value={d['value']:.1f} step={d['ms_per_step']*1e3:.1f}us {ks} x={x and round(x['total_ms']*1e3/x['calls'])}")
+x=d['exchange'] if d.get('exchange') and 'nccl_calls' in d['exchange'] else None
+print(f"{sys.argv[2]:45s} value={d['value']:.1f} step={d['ms_per_step']*1e3:.1f}us {ks} x={x and round(x['nccl_total_ms']*1e3/x['nccl_calls'])}")
 PY
 done

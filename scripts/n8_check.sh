@@ -12,8 +12,8 @@ f=f"gpurun_out/n8_{sys.argv[1]}_{sys.argv[2]}.log"
 l=[x for x in open(f) if x.startswith("{")]
 if not l: print(sys.argv[1:], open(f).read()[-2500:]); sys.exit()
 d=json.loads(l[-1]); ks=" ".join(f"{k}={v['avg_us']:.1f}us" for k,v in d["kernels"].items())
-x=d['exchange']
-print(f"N={sys.argv[1]} {sys.argv[2]:9s} value={d['value']:.1f} step={d['ms_per_step']*1e3:.1f}us {ks} x_us={x and round(x['total_ms']*1e3/x['calls'])} waits={d.get('waits')}")
+x=d['exchange'] if d.get('exchange') and 'nccl_calls' in d['exchange'] else None
+print(f"N={sys.argv[1]} {sys.argv[2]:9s} value={d['value']:.1f} step={d['ms_per_step']*1e3:.1f}us {ks} x_us={x and round(x['nccl_total_ms']*1e3/x['nccl_calls'])} waits={d.get('waits')}")
 PY
 done
 done

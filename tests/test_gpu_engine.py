@@ -239,3 +239,33 @@ def test_round_payloads_to_reference_frames(pkg):
         else:
             with pytest.raises(E.ConfigError):
                 wk.round_payloads(t)
+
+
+def test_module_integration_matches_oracle(pkg):
+    """A torch MLP trained through CDSGDModule: the gradients autograd produced at the
+    engine's compute weights, replayed through the lock-step oracle, give the same
+    residuals (bitwise) and weights (tolerance) — the plumbing (key order, grad views,
+    compute-weight reloads) is exact."""
+    from paper_2106_10796_b200.model import CDSGDModule
+
+    _, E, L, _ = pkg
+    torch.manual_seed(0)
+    net = torch.nn.Sequential(torch.nn.Linear(20, 33), torch.nn.Tanh(), torch.nn.Linear(33, 3)).cuda()
+    hp = E.HyperParams(algo="cdsgd", workers=1, eta_global=0.05, eta_local=0.2, k=3, alpha=0.05, warmup_n=2)
+    m = CDSGDModule(net, hp)
+    sizes = m.layout.lengths
+    w0 = torch.cat([p.detach().reshape(-1) for p in net.parameters()]).double().cpu().numpy()
+    orc = O.LockstepOracle(w0, sizes, O.OracleHP("cdsgd", 1, 0.05, 0.2, 3, 0.05, 2))
+    x = torch.randn(64, 20, device="cuda")
+    y = torch.randint(0, 3, (64,), device="cuda")
+    for t in range(10):
+        cw = torch.cat([p.detach().reshape(-1) for p in net.parameters()]).cpu().numpy()
+        np.testing.assert_allclose(cw, orc.compute_weights(0), rtol=RTOL, atol=ATOL, err_msg=f"round {t}")
+        torch.nn.functional.cross_entropy(net(x[t * 6:t * 6 + 6]), y[t * 6:t * 6 + 6]).backward()
+        g = torch.cat([p.grad.reshape(-1) for p in net.parameters()]).cpu().numpy()
+        m.step()
+        orc.step([g])
+        assert np.array_equal(bits(m.worker.residual.cpu().numpy()), bits(orc.workers[0].residual)), t
+    m.flush()
+    W = torch.cat([p.detach().reshape(-1) for p in net.parameters()]).cpu().numpy()
+    np.testing.assert_allclose(W, orc.W, rtol=RTOL, atol=ATOL)
