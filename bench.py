@@ -286,6 +286,8 @@ def run_ours(args):
         "local_update": 3 * 4 * n,
         # apply(t-1) + quantize(t): g 4 | r 8+8 | W 4+4 | loc 4 | codes in N/4 + out 1/4
         "fused": 4 * n + 16 * n + 8 * n + 4 * n + world * 4 * nw + 4 * nw,
+        # quantize(t) + loc_{t+1} = W_t - eta_l*g_t (nothing to apply): g 4 | r 8+8 | W 4 | loc 4 | codes 1/4
+        "fused_local": 4 * n + 16 * n + 4 * n + 4 * n + 4 * nw,
         # P2P correction: stage g (4+4); reduce of my shard n/N: N stage reads + W r/w (+ N-1 remote W writes)
         "stage": 8 * n,
         "reduce": (world * 4 * n + 4 * n + world * 4 * n) // max(world, 1),

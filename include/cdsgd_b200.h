@@ -223,12 +223,12 @@ int cdsgd_engine_attach_p2p(cdsgd_engine* eng, void* const* peer_bases, int32_t 
 int cdsgd_engine_join(cdsgd_engine* eng, void* stream);
 /* Per-kernel timing with CUDA events recorded on the launching streams around
  * each K1 / K2 / K3 / local-update launch and each NCCL call, between _begin and
- * _end. _end synchronises and writes 18 doubles, (ms, launches) per class:
+ * _end. _end synchronises and writes 20 doubles, (ms, launches) per class:
  * quantize, apply_quant, apply_full, local_update, exchange (NCCL), fused
  * (apply(t-1) + quantize(t) in one kernel), stage, reduce (P2P correction), wait
- * (P2P correction completion). */
+ * (P2P correction completion), fused_local (quantize(t) + local update only). */
 int cdsgd_engine_profile_begin(cdsgd_engine* eng);
-int cdsgd_engine_profile_end(cdsgd_engine* eng, double* out18);
+int cdsgd_engine_profile_end(cdsgd_engine* eng, double* out20);
 
 #ifdef __cplusplus
 }

@@ -385,7 +385,8 @@ int launch_apply_quant(const cdsgd_layout* L, float* W, const uint32_t* gathered
                        double alpha, double eta_g, const float* gnext, float* loc, double eta_l, uint64_t* err,
                        uint64_t skip_below, double* gnorm, const DecodeTab* tab_in, int exact_in,
                        cudaStream_t st, const P2PArgs* x = nullptr, float* gstage = nullptr,
-                       const P2PArgs* xs = nullptr, unsigned int* sched = nullptr) {
+                       const P2PArgs* xs = nullptr, unsigned int* sched = nullptr, float fold_scale = 0.f,
+                       double* gnorm2 = nullptr) {
     if (L == nullptr) return fail(CDSGD_ERR_ARG, "layout is NULL");
     if (nr < 1 || nr > MAX_RANKS - 1) return fail(CDSGD_ERR_ARG, "nranks must be in [1, %d]", MAX_RANKS - 1);
     if ((gnext == nullptr) != (loc == nullptr)) return fail(CDSGD_ERR_ARG, "g_next and loc_out go together");
@@ -409,6 +410,8 @@ int launch_apply_quant(const cdsgd_layout* L, float* W, const uint32_t* gathered
     a.gstage = gstage;
     a.xs = xs != nullptr ? *xs : P2PArgs{};
     a.sched = sched;
+    a.fold_scale = fold_scale;
+    a.gnorm2 = gnorm2;
     DecodeTab tab;
     int exact;
     if (tab_in != nullptr) {
@@ -596,7 +599,7 @@ struct cdsgd_engine {
     bool pcorr = false;                // P2P mode: correction rounds by the exact sharded NVLink reduce
     bool diag_local_codes = false;     // timing diagnostic: store codes only locally
     // profiling: event pairs per kernel class (0 quant, 1 apply_q, 2 apply_f, 3 local, 4 exchange, 5 fused,
-    // 6 stage, 7 reduce, 8 wait)
+    // 6 stage, 7 reduce, 8 wait, 9 fused local-only)
     bool prof = false;
     std::vector<cudaEvent_t> ev_pool;
     size_t ev_used = 0;
@@ -766,7 +769,7 @@ int p2p_reduce_async(cdsgd_engine* E, int64_t t, cudaStream_t C) {
 // Finish round p: wait for its exchange, then K2 (codes) or K3 (full) fused with
 // the local update from g_next (nullable).
 int engine_apply(cdsgd_engine* E, int64_t p, bool comp, const float* gp, const float* gnext, cudaStream_t C,
-                 float* gstage = nullptr, const P2PArgs* xs = nullptr) {
+                 float* gstage = nullptr, const P2PArgs* xs = nullptr, bool fold = false) {
     const int nr = E->d.nranks;
     if (!comp && E->p2p && E->pcorr) {  // P2P correction: exact sharded reduce, then (optionally) the local update
         int rc = CDSGD_OK;
@@ -800,11 +803,17 @@ int engine_apply(cdsgd_engine* E, int64_t p, bool comp, const float* gp, const f
             x.counter = E->counters + 1;
             x.err = E->d.err;
         }
+        double* gn2 = nullptr;  // grad-norm slot of the folded correction round p+1
+        if (fold && E->d.gnorm_sq != nullptr && E->d.gnorm_ring > 0) {
+            gn2 = E->d.gnorm_sq + ((p + 1) % E->d.gnorm_ring);
+            CUDA_TRY(cudaMemsetAsync(gn2, 0, sizeof(double), C));
+        }
         const long pi = prof_start(E, 1, C);
         const int rc = launch_apply_quant(E->L, E->d.weights, E->d.gathered[p & 1], nr, words_of(E), E->d.alpha,
                                           E->d.eta_global, gnext, loc, E->d.eta_local, E->d.err, skip_below, gn,
                                           &E->tab, E->exact, C, &x, gstage, xs,
-                                          E->sched != nullptr ? E->sched + 2 : nullptr);
+                                          E->sched != nullptr ? E->sched + 2 : nullptr,
+                                          fold ? static_cast<float>(E->d.eta_global) : 0.f, gn2);
         prof_stop(E, pi, C);
         return rc;
     }
@@ -977,7 +986,7 @@ extern "C" int cdsgd_engine_profile_begin(cdsgd_engine* E) {
 extern "C" int cdsgd_engine_profile_end(cdsgd_engine* E, double* out) {
     if (E == nullptr || out == nullptr) return fail(CDSGD_ERR_ARG, "NULL argument");
     E->prof = false;
-    for (int i = 0; i < 18; ++i) out[i] = 0.0;
+    for (int i = 0; i < 20; ++i) out[i] = 0.0;
     for (const auto& m : E->prof_marks) {
         CUDA_TRY(cudaEventSynchronize(E->ev_pool[m.second + 1]));
         float ms = 0.f;
@@ -1076,9 +1085,12 @@ extern "C" int cdsgd_engine_step(cdsgd_engine* E, const float* g, void* stream) 
         E->t = t + 1;
         return CDSGD_OK;
     }
-    if (E->fuse && comp && E->pending && !sync_path0 && (E->pend_comp || nr == 1)) {
-        // ---- one kernel: apply(t-1) fused with quantize(t); both read g_t once
-        const int64_t pnd = E->pend_t;
+    if (E->fuse && comp && !sync_path0 && (E->pending ? (E->pend_comp || nr == 1) : nr == 1)) {
+        // ---- one kernel: apply(t-1) fused with quantize(t); both read g_t once. With nothing
+        // pending (first local round, or N=1 after a folded correction) the apply part is just
+        // loc_{t+1} = W_t - eta_l*g_t.
+        const bool has_pend = E->pending;
+        const int64_t pnd = has_pend ? E->pend_t : t;
         FusedArgs a{};
         a.g = g;
         a.r_in = E->d.residual[E->rcur];
@@ -1098,10 +1110,11 @@ extern "C" int cdsgd_engine_step(cdsgd_engine* E, const float* g, void* stream) 
         a.skip_below = rel <= 0 ? 0ull : (static_cast<uint64_t>(rel) << CDSGD_INDEX_BITS);
         a.err = E->d.err;
         a.sched = E->sched;
-        if (E->d.gnorm_sq != nullptr && E->d.gnorm_ring > 0) {
+        if (has_pend && E->d.gnorm_sq != nullptr && E->d.gnorm_ring > 0) {
             a.gnorm = E->d.gnorm_sq + (pnd % E->d.gnorm_ring);
             CUDA_TRY(cudaMemsetAsync(a.gnorm, 0, sizeof(double), C));
         }
+        if (!has_pend) a.skip_below = 0;
         if (E->p2p) {
             const int p = static_cast<int>(t & 1), q = static_cast<int>(pnd & 1);
             char* local = E->peer[E->d.rank];
@@ -1125,8 +1138,8 @@ extern "C" int cdsgd_engine_step(cdsgd_engine* E, const float* g, void* stream) 
             E->last_use[p] = t;
         }
         E->rlog.push_back(static_cast<int8_t>(E->rcur));
-        const long pi = prof_start(E, 5, C);
-        rc = launch_fused(nr, E->pend_comp ? APPLY_Q : APPLY_F, a, E->L->tab(), E->tab, C);
+        const long pi = prof_start(E, has_pend ? 5 : 9, C);
+        rc = launch_fused(nr, !has_pend ? APPLY_L : (E->pend_comp ? APPLY_Q : APPLY_F), a, E->L->tab(), E->tab, C);
         prof_stop(E, pi, C);
         if (rc != CDSGD_OK) return rc;
         E->rcur ^= 1;
@@ -1210,6 +1223,14 @@ extern "C" int cdsgd_engine_step(cdsgd_engine* E, const float* g, void* stream) 
             prepare_stage(E, t, &dst, &xs);
             rc = engine_apply(E, E->pend_t, E->pend_comp, E->pend_grad, g, C, dst, &xs);
             staged = true;
+        } else if (E->pending && !comp && nr == 1 && E->pend_comp && E->fuse) {
+            // N=1: this correction round's mean is g_t itself -> apply it in the same pass
+            rc = engine_apply(E, E->pend_t, true, E->pend_grad, g, C, nullptr, nullptr, /*fold=*/true);
+            if (rc != CDSGD_OK) return rc;
+            E->pending = false;
+            E->compute_is_loc = true;
+            E->t = t + 1;
+            return CDSGD_OK;
         } else if (E->pending) {
             rc = engine_apply(E, E->pend_t, E->pend_comp, E->pend_grad, g, C);
         } else {

@@ -332,6 +332,11 @@ struct ApplyQArgs {
     float* gstage;  // non-null: also copy g_next here (staging of a P2P correction round)
     P2PArgs xs;     // staging protocol: wait gfreed, publish gready
     unsigned int* sched;  // [2] dynamic tile scheduler {next tile, CTAs done}; nullptr = static ranges
+    // N=1, the round after this one is a correction whose mean is g_next itself: also apply
+    // it here, W <- fma(-fold_scale, g_next, W) after the local update (fold_scale = eta_g/1),
+    // with its grad-norm into gnorm2. 0 = off.
+    float fold_scale;
+    double* gnorm2;
 };
 
 __device__ __forceinline__ double apply_mean_general(const uint32_t* codes, int nr, double alpha,
@@ -361,7 +366,7 @@ __global__ void __launch_bounds__(256) k_apply_quant(ApplyQArgs a, KeyTab kt, De
     int64_t tb, te;
     warp_range(kt.ntiles, tb, te);
     const int lane = threadIdx.x & 31;
-    double gsq = 0.0;
+    double gsq = 0.0, gsq2 = 0.0;
     int isq = 0;  // sum of cnt^2 on the table path: gsq += isq * (alpha/N)^2
     uint64_t bad_idx = NO_ERR;
     const bool do_loc = a.loc != nullptr;
@@ -428,6 +433,11 @@ __global__ void __launch_bounds__(256) k_apply_quant(ApplyQArgs a, KeyTab kt, De
                         w4[q] = __fsub_rn(w4[q], s_upd[cq[q] + nr]);
                         if (do_loc) l4[q] = __fmaf_rn(-a.eta_l, g4[q], w4[q]);
                         isq += cq[q] * cq[q];
+                        if (a.fold_scale != 0.f) {  // N=1 correction round t+1: W_{t+2} = W_{t+1} - eta*g_{t+1}
+                            w4[q] = __fmaf_rn(-a.fold_scale, g4[q], w4[q]);
+                            const double m = static_cast<double>(g4[q]);
+                            gsq2 = __fma_rn(m, m, gsq2);
+                        }
                     }
                     if (((cnt.rsv >> (2 * jb)) & 0xffu) != 0u) {
                         const int q = __ffs((cnt.rsv >> (2 * jb)) & 0x55u) / 2;
@@ -466,9 +476,14 @@ __global__ void __launch_bounds__(256) k_apply_quant(ApplyQArgs a, KeyTab kt, De
                             mean = apply_mean_general(codes, nr, a.alpha, a.inv_n_or_zero, rsv);
                             upd = __double2float_rn(__dmul_rn(a.eta_g_d, mean));
                         }
-                        const float wn = __fsub_rn(a.W[e], upd);
-                        a.W[e] = wn;
+                        float wn = __fsub_rn(a.W[e], upd);
                         if (do_loc) a.loc[e] = __fmaf_rn(-a.eta_l, a.gnext[e], wn);
+                        if (a.fold_scale != 0.f) {
+                            const float gn = a.gnext[e];
+                            wn = __fmaf_rn(-a.fold_scale, gn, wn);
+                            gsq2 = __fma_rn(static_cast<double>(gn), static_cast<double>(gn), gsq2);
+                        }
+                        a.W[e] = wn;
                         if (a.gstage != nullptr) a.gstage[e] = a.gnext[e];
                         if (a.gnorm != nullptr) gsq = __fma_rn(mean, mean, gsq);
                         if (rsv) bad_idx = static_cast<uint64_t>(e) < bad_idx ? static_cast<uint64_t>(e) : bad_idx;
@@ -482,6 +497,11 @@ __global__ void __launch_bounds__(256) k_apply_quant(ApplyQArgs a, KeyTab kt, De
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) gsq += __shfl_xor_sync(FULL, gsq, o);
         if (lane == 0 && gsq != 0.0) atomicAdd(a.gnorm, gsq);
+    }
+    if (a.gnorm2 != nullptr) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) gsq2 += __shfl_xor_sync(FULL, gsq2, o);
+        if (lane == 0 && gsq2 != 0.0) atomicAdd(a.gnorm2, gsq2);
     }
     if (a.err != nullptr) {
         bad_idx = warp_min_u64(bad_idx);

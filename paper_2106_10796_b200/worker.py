@@ -258,10 +258,10 @@ class CDSGDWorker:
 
     def profile_end(self) -> dict:
         """Per-kernel-class total ms and launch counts since profile_begin()."""
-        out = (C.c_double * 18)()
+        out = (C.c_double * 20)()
         _lib.check(self._lib.cdsgd_engine_profile_end(self._eng, out), "profile_end")
         names = ("quantize", "apply_quant", "apply_full", "local_update", "exchange", "fused", "stage", "reduce",
-                 "wait")
+                 "wait", "fused_local")
         return {nm: {"ms": out[2 * i], "n": int(out[2 * i + 1])} for i, nm in enumerate(names)}
 
     def close(self) -> None:
