@@ -53,6 +53,7 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="budget of the cpu_baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-secondary", action="store_true", help="skip the ResNet-20 (configs[1]) line at N=1")
     return ap.parse_args()
 
 
@@ -208,6 +209,38 @@ def run_reference(args):
 
 
 # ----------------------------------------------------------------------------- our arm
+
+
+def small_layout_rate(args, dev, name="resnet20", steps=400, warmup=20):
+    """Device-timed throughput of one worker on a small layout (launch/latency-bound)."""
+    import torch
+
+    from paper_2106_10796_b200.engine import HyperParams
+    from paper_2106_10796_b200.layout import by_name
+    from paper_2106_10796_b200.worker import CDSGDWorker
+
+    layout = by_name(name)
+    n = layout.total
+    gen = torch.Generator(device=dev).manual_seed(7)
+    pool = [0.3 * torch.randn(n, device=dev, generator=gen) for _ in range(2)]
+    wk = CDSGDWorker(layout, HyperParams(algo="cdsgd", workers=1, eta_global=0.1, eta_local=0.4, k=args.k,
+                                         alpha=args.alpha, warmup_n=0), torch.zeros(n, device=dev))
+    for i in range(warmup):
+        wk.step(pool[i % 2])
+    torch.cuda.synchronize(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for i in range(steps):
+        wk.step(pool[(warmup + i) % 2])
+    e1.record()
+    e1.synchronize()
+    ms = e0.elapsed_time(e1)
+    wk.check()
+    wk.close()
+    return {"workload": f"{name}-sized gradient: {len(layout)} keys, {n:,} fp32 elements", "metric": METRIC,
+            "value": n * steps / (ms / 1e3) / 1e9, "unit": UNIT, "steps": steps, "ms_per_step": ms / steps,
+            "note": "BASELINE configs[1]; inputs stay L2-resident at this size (latency-bound)"}
+
 
 
 def run_ours(args):
@@ -369,6 +402,12 @@ def run_ours(args):
                "path": "CDSGDWorker.step (public API -> C ABI) with the gradient copied from pinned host memory "
                        "on a copy stream each step and the round's grad-norm read back to pinned host"}
 
+    # configs[1] of BASELINE.json: the ResNet-20/CIFAR-10-sized gradient on one B200
+    # (quantize + apply kernels only) — measured beside the headline when N=1
+    secondary = None
+    if world == 1 and args.workload == "resnet50" and not args.no_secondary:
+        secondary = {"resnet20": small_layout_rate(args, dev)}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(layout, args, 1)
@@ -389,6 +428,7 @@ def run_ours(args):
                        "l2": f"inputs larger than L2: {(20 * n) / 2**20:.0f} MiB touched per step per rank",
                        "parallelism": f"dp{world}"},
             "roofline": roof, "kernels": kernels, "waits": waits, "exchange": exch, "cpu_baseline": cpu, "e2e": e2e,
+            "secondary": secondary,
             "gpu_launches": launches, "clocks": clk,
         }
         print(json.dumps(line), flush=True)

@@ -463,7 +463,12 @@ int launch_apply_full(float* W, const float* gsum, int nr, int64_t n, double eta
 // Fused apply(t-1) + quantize(t), register-staged (measured faster than a TMA-ring variant).
 template <int NR, int AP>
 int launch_fused_cfg(const FusedArgs& a, const KeyTab& kt, const DecodeTab& tab, cudaStream_t st) {
-    k_fused_ldg<NR, AP><<<tile_grid(k_fused_ldg<NR, AP>, kt.ntiles), THREADS, 0, st>>>(a, kt, tab);
+    // fewer than 2 whole-tile tasks per resident warp: split tiles into chunk tasks
+    const int64_t warps = static_cast<int64_t>(resident_blocks(k_fused_ldg<NR, AP, CHUNKS>, THREADS)) * WARPS_PER_BLOCK;
+    if (kt.ntiles < 2 * warps)
+        k_fused_ldg<NR, AP, 1><<<tile_grid(k_fused_ldg<NR, AP, 1>, kt.ntiles * CHUNKS), THREADS, 0, st>>>(a, kt, tab);
+    else
+        k_fused_ldg<NR, AP, CHUNKS><<<tile_grid(k_fused_ldg<NR, AP, CHUNKS>, kt.ntiles), THREADS, 0, st>>>(a, kt, tab);
     return CDSGD_OK;
 }
 int launch_fused(int nr, int apply, const FusedArgs& a, const KeyTab& kt, const DecodeTab& tab, cudaStream_t st) {

@@ -47,8 +47,11 @@ struct FusedArgs {
 
 // Data moved with 128/256-bit coalesced loads straight into registers (all loads of a
 // tile issued first), two 256-thread CTAs per SM, dynamic tile scheduling.
-template <int NR, int APPLY>
+// CH = chunks of 128 elements per task: 4 (a whole tile) for large layouts, 1 for small
+// ones (ResNet-20-sized), where 4x more warps in flight beat the per-tile latency chain.
+template <int NR, int APPLY, int CH = CHUNKS>
 __global__ void __launch_bounds__(256, 2) k_fused_ldg(FusedArgs a, KeyTab kt, DecodeTab tab) {
+    constexpr int SPL = CHUNKS / CH;  // tasks per tile
     __shared__ float s_upd[2 * MAX_RANKS + 1];
     p2p_wait2(a.xq, a.xa);
     const uint64_t e0v = a.err != nullptr ? *reinterpret_cast<volatile uint64_t*>(a.err) : ~0ull;
@@ -59,40 +62,43 @@ __global__ void __launch_bounds__(256, 2) k_fused_ldg(FusedArgs a, KeyTab kt, De
     const int lane = threadIdx.x & 31;
     const uint32_t ahi = static_cast<uint32_t>(__double2hiint(a.alpha));
     const uint32_t alo = static_cast<uint32_t>(__double2loint(a.alpha));
+    const int64_t ntasks = kt.ntiles * SPL;
     int64_t tb, te;
-    warp_range(kt.ntiles, tb, te);
+    warp_range(ntasks, tb, te);
     uint64_t bad_idx = NO_ERR, bad_sym = NO_ERR;
     double gsq = 0.0;
     int isq = 0;
-    // Dynamic schedule: warps claim CLAIM consecutive tiles at a time from a global ticket,
+    // Dynamic schedule: warps claim CLAIM consecutive tasks at a time from a global ticket,
     // so the kernel ends when the work does, not when the slowest static range does.
-    // small layouts (fewer than ~4 tiles per warp): claim single tiles for parallelism
-    const unsigned CLAIM = kt.ntiles < 4 * ((int64_t)gridDim.x * blockDim.x / 32) ? 1u : 2u;
+    // small layouts (fewer than ~4 tasks per warp): claim single tasks for parallelism
+    const unsigned CLAIM = ntasks < 4 * ((int64_t)gridDim.x * blockDim.x / 32) ? 1u : 2u;
     const bool dyn = a.sched != nullptr;
     int64_t cbase = 0, cend = 0;
     if (dyn) {
         unsigned t0 = 0;
         if (lane == 0) t0 = atomicAdd(a.sched, CLAIM);
         cbase = __shfl_sync(FULL, t0, 0);
-        cend = cbase + (int64_t)CLAIM < kt.ntiles ? cbase + (int64_t)CLAIM : kt.ntiles;
+        cend = cbase + (int64_t)CLAIM < ntasks ? cbase + (int64_t)CLAIM : ntasks;
         tb = cbase;
-        te = cbase < kt.ntiles ? kt.ntiles : cbase;  // loop bound; real bound checked per claim
+        te = cbase < ntasks ? ntasks : cbase;  // loop bound; real bound checked per claim
     }
     if (tb < te) {
         TileCursor cc;
-        cc.seek(kt, tb);
-        for (int64_t ti = tb; ti < te; ++ti) {
+        cc.seek(kt, tb / SPL);
+        for (int64_t task = tb; task < te; ++task) {
             if (dyn) {
-                if (ti >= cend) {  // claim the next batch
+                if (task >= cend) {  // claim the next batch
                     unsigned t0 = 0;
                     if (lane == 0) t0 = atomicAdd(a.sched, CLAIM);
                     const int64_t nb = __shfl_sync(FULL, t0, 0);
-                    if (nb >= kt.ntiles) break;
-                    ti = nb;
-                    cend = nb + (int64_t)CLAIM < kt.ntiles ? nb + (int64_t)CLAIM : kt.ntiles;
-                    if (ti < cc.t0) cc.seek(kt, ti);
+                    if (nb >= ntasks) break;
+                    task = nb;
+                    cend = nb + (int64_t)CLAIM < ntasks ? nb + (int64_t)CLAIM : ntasks;
                 }
             }
+            const int64_t ti = task / SPL;
+            const int c0 = static_cast<int>(task % SPL) * CH;  // first chunk of this task
+            if (ti < cc.t0) cc.seek(kt, ti);
             cc.advance_to(kt, ti);
             const int64_t j = ti - cc.t0;
             const int64_t e0 = cc.e0 + j * TILE_ELEMS;
@@ -104,28 +110,29 @@ __global__ void __launch_bounds__(256, 2) k_fused_ldg(FusedArgs a, KeyTab kt, De
             const bool fast = ne == TILE_ELEMS && aligned_to(a.g + e0, 16) && aligned_to(a.r_in + e0, 32) &&
                               aligned_to(a.r_out + e0, 32) && aligned_to(a.W + e0, 16) && aligned_to(a.loc + e0, 16) &&
                               (APPLY != APPLY_F || aligned_to(a.gsum + e0, 16));
+            if (!fast && c0 != 0) continue;  // partial / misaligned tiles: one task does the whole tile
             uint32_t myword = 0;
             if (fast) {
-                float4 gv[CHUNKS], wv[CHUNKS], sv[CHUNKS];
-                d4 rv[CHUNKS];
+                float4 gv[CH], wv[CH], sv[CH];
+                d4 rv[CH];
                 uint32_t cw[APPLY == APPLY_Q ? NR : 1];
                 if constexpr (APPLY == APPLY_Q) {
 #pragma unroll
                     for (int r = 0; r < NR; ++r) cw[r] = ld_word(a.gathered + r * a.stride + w0 + lane);
                 }
 #pragma unroll
-                for (int c = 0; c < CHUNKS; ++c) {
-                    const int64_t e = e0 + 128 * c + 4 * lane;
+                for (int c = 0; c < CH; ++c) {
+                    const int64_t e = e0 + 128 * (c0 + c) + 4 * lane;
                     gv[c] = ld_stream(a.g + e);
                     rv[c] = ld_stream(a.r_in + e);
                     wv[c] = ld_stream(a.W + e);
                     if constexpr (APPLY == APPLY_F) sv[c] = ld_stream(a.gsum + e);
                 }
-                uint32_t v[CHUNKS];
+                uint32_t v[CH];
                 bool bad = false;
 #pragma unroll
-                for (int c = 0; c < CHUNKS; ++c) {
-                    const int64_t e = e0 + 128 * c + 4 * lane;
+                for (int c = 0; c < CH; ++c) {
+                    const int64_t e = e0 + 128 * (c0 + c) + 4 * lane;
                     float g4[4] = {gv[c].x, gv[c].y, gv[c].z, gv[c].w};
                     float w4[4] = {wv[c].x, wv[c].y, wv[c].z, wv[c].w};
                     double r4[4] = {rv[c].x, rv[c].y, rv[c].z, rv[c].w};
@@ -134,7 +141,7 @@ __global__ void __launch_bounds__(256, 2) k_fused_ldg(FusedArgs a, KeyTab kt, De
                         if constexpr (APPLY == APPLY_Q) {
                             Counts cnt{0u, 0u, 0u, 0u, 0u};
 #pragma unroll
-                            for (int r = 0; r < NR; ++r) count_add(cnt, __shfl_sync(FULL, cw[r], 8 * c + (lane >> 2)));
+                            for (int r = 0; r < NR; ++r) count_add(cnt, __shfl_sync(FULL, cw[r], 8 * (c0 + c) + (lane >> 2)));
                             int cq[4];
                             lane_counts(cnt, lane, cq);
 #pragma unroll
@@ -179,25 +186,26 @@ __global__ void __launch_bounds__(256, 2) k_fused_ldg(FusedArgs a, KeyTab kt, De
                 }
                 if (__any_sync(FULL, bad)) {
 #pragma unroll
-                    for (int c = 0; c < CHUNKS; ++c) {
+                    for (int c = 0; c < CH; ++c) {
                         const float g4[4] = {gv[c].x, gv[c].y, gv[c].z, gv[c].w};
                         const double r4[4] = {rv[c].x, rv[c].y, rv[c].z, rv[c].w};
 #pragma unroll
                         for (int q = 0; q < 4; ++q)
                             if (nonfinite(__dadd_rn(r4[q], static_cast<double>(g4[q])))) {
-                                const uint64_t idx = a.tag | static_cast<uint64_t>(e0 + 128 * c + 4 * lane + q);
+                                const uint64_t idx =
+                                    a.tag | static_cast<uint64_t>(e0 + 128 * (c0 + c) + 4 * lane + q);
                                 bad_idx = idx < bad_idx ? idx : bad_idx;
                             }
                     }
                 }
 #pragma unroll
-                for (int c = 0; c < CHUNKS; ++c) v[c] |= __shfl_xor_sync(FULL, v[c], 1);
+                for (int c = 0; c < CH; ++c) v[c] |= __shfl_xor_sync(FULL, v[c], 1);
 #pragma unroll
-                for (int c = 0; c < CHUNKS; ++c) v[c] |= __shfl_xor_sync(FULL, v[c], 2);
+                for (int c = 0; c < CH; ++c) v[c] |= __shfl_xor_sync(FULL, v[c], 2);
 #pragma unroll
-                for (int c = 0; c < CHUNKS; ++c) {
+                for (int c = 0; c < CH; ++c) {
                     const uint32_t w = __shfl_sync(FULL, v[c], 4 * (lane & 7));
-                    if ((lane >> 3) == c) myword = w;
+                    if ((lane >> 3) == c0 + c) myword = w;
                 }
             } else {
                 uint32_t cw[APPLY == APPLY_Q ? NR : 1];
@@ -257,7 +265,8 @@ __global__ void __launch_bounds__(256, 2) k_fused_ldg(FusedArgs a, KeyTab kt, De
                     if (lane == 2 * s + 1) myword = interleave_codes(pm >> 16, mm >> 16);
                 }
             }
-            if (lane < nw && !q_off) {
+            const bool mine_word = !fast || ((lane >> 3) >= c0 && (lane >> 3) < c0 + CH);
+            if (lane < nw && !q_off && mine_word) {
                 if (a.xq.nranks > 0) {
                     for (int r = 0; r < a.xq.nranks; ++r) a.xq.dst[r][w0 + lane] = myword;
                 } else {

@@ -31,6 +31,7 @@ RTOL, ATOL = 1e-5, 1e-6
 
 CASES = [
     # algo, sizes, k, warmup, iters, alpha
+    ("cdsgd", [2_600_000, 513], 4, 0, 7, 0.5),  # whole-tile (CH=4) path of the fused kernel
     ("cdsgd", [1000, 37, 16, 1, 4096], 4, 5, 14, 0.5),
     ("cdsgd", [2048, 513], 2, 0, 9, 0.5),
     ("cdsgd", [777], 3, 1, 9, 0.3),

@@ -38,6 +38,8 @@ def pkg():
 
 CASES = [
     # algo, sizes, k, warmup, iters, alpha, force, bypass
+    # > 2 tiles per resident warp: the whole-tile (CH=4) path of the fused kernel
+    ("cdsgd", [3_000_000, 4099, 17], 4, 1, 9, 0.5, False, False),
     ("cdsgd", [1000, 37, 16, 1], 4, 5, 16, 0.5, False, False),
     ("cdsgd", [300], 3, 0, 12, 0.5, False, False),
     ("cdsgd", [4099, 512, 3], 2, 1, 11, 0.5, False, False),
