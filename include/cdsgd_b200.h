@@ -177,7 +177,7 @@ typedef struct {
     uint32_t* gathered[2];   /* [nranks * words] each */
     float* gsum[2];          /* [n] fp32 each (nranks > 1; may be NULL when nranks == 1) */
     uint64_t* err;           /* [2] device words, init CDSGD_NO_ERROR */
-    double* gnorm_sq;        /* [gnorm_ring] device, nullable */
+    double* gnorm_sq;        /* [gnorm_ring] device, nullable; zeroed by create, round t valid for ring-2 rounds */
 } cdsgd_engine_desc;
 
 typedef struct {

@@ -92,6 +92,31 @@ int flat_grid(K kernel, int64_t work) {
 }
 inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
+// Engine-path kernels are launched with programmatic stream serialization: the next
+// round's grid is scheduled while this one drains and blocks in pdl_enter() until it has
+// completed (kernels.cuh). CDSGD_NO_PDL=1 launches them plainly (A/B knob).
+bool pdl_on() {
+    static const bool v = [] {
+        const char* e = getenv("CDSGD_NO_PDL");
+        return !(e != nullptr && e[0] == '1');
+    }();
+    return v;
+}
+template <typename... P, typename... A>
+void launch_pdl(void (*kernel)(P...), int grid, int block, size_t smem, cudaStream_t st, A&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_on() ? 1 : 0;
+    (void)cudaLaunchKernelEx(&cfg, kernel, std::forward<A>(args)...);  // errors: cudaGetLastError
+}
+
 // TMA-staged kernels (K1, K3): one CTA per SM, dynamic smem ring.
 template <typename K>
 bool prepare_tma(K kernel, int smem_bytes) {
@@ -133,7 +158,7 @@ int launch_af_tma(const ApplyFArgs& a, cudaStream_t st) {
     using SM = ApplyFSmem<WP, ST>;
     static_assert(SM::BYTES <= 227 * 1024, "smem");
     if (!prepare_tma(k_apply_full_tma<WP, ST>, SM::BYTES)) return fail(CDSGD_ERR_CUDA, "smem attribute");
-    k_apply_full_tma<WP, ST><<<tma_grid((a.n + TILE_ELEMS - 1) / TILE_ELEMS, WP), WP * 32, SM::BYTES, st>>>(a);
+    launch_pdl(k_apply_full_tma<WP, ST>, tma_grid((a.n + TILE_ELEMS - 1) / TILE_ELEMS, WP), WP * 32, SM::BYTES, st, a);
     return CDSGD_OK;
 }
 int launch_af_tma_cfg(const ApplyFArgs& a, cudaStream_t st) {
@@ -149,8 +174,8 @@ int launch_quant_tma(const G* g, const double* r_in, double* r_out, uint32_t* wo
     using SM = QuantSmem<G, WARPS, ST>;
     static_assert(SM::BYTES <= 227 * 1024, "smem");
     if (!prepare_tma(k_quantize_tma<G, WARPS, ST>, SM::BYTES)) return fail(CDSGD_ERR_CUDA, "smem attribute");
-    k_quantize_tma<G, WARPS, ST><<<tma_grid(kt.ntiles, WARPS), WARPS * 32, SM::BYTES, st>>>(g, r_in, r_out, words, kt,
-                                                                                          alpha, err, tag, x);
+    launch_pdl(k_quantize_tma<G, WARPS, ST>, tma_grid(kt.ntiles, WARPS), WARPS * 32, SM::BYTES, st, g, r_in, r_out,
+               words, kt, alpha, err, tag, x);
     return CDSGD_OK;
 }
 template <typename G>
@@ -339,8 +364,8 @@ extern "C" int cdsgd_local_update(const void* base, int32_t bdt, const void* g, 
     if (n == 0) return CDSGD_OK;
     if (bdt < 0 || bdt > 1 || gdt < 0 || gdt > 1 || odt < 0 || odt > 1) return fail(CDSGD_ERR_ARG, "bad dtype");
 #define LU(TB, TG, TO)                                                                                   \
-    k_local_update<TB, TG, TO><<<flat_grid(k_local_update<TB, TG, TO>, n), THREADS, 0, S(stream)>>>(   \
-        static_cast<const TB*>(base), static_cast<const TG*>(g), static_cast<TO*>(out), n, eta_l)
+    launch_pdl(k_local_update<TB, TG, TO>, flat_grid(k_local_update<TB, TG, TO>, n), THREADS, 0, S(stream), \
+               static_cast<const TB*>(base), static_cast<const TG*>(g), static_cast<TO*>(out), n, eta_l)
     const int code = bdt * 4 + gdt * 2 + odt;
     switch (code) {
         case 0: LU(float, float, float); break;
@@ -384,9 +409,9 @@ inline bool pow2(int n) { return n > 0 && (n & (n - 1)) == 0; }
 int launch_apply_quant(const cdsgd_layout* L, float* W, const uint32_t* gathered, int nr, int64_t stride,
                        double alpha, double eta_g, const float* gnext, float* loc, double eta_l, uint64_t* err,
                        uint64_t skip_below, double* gnorm, const DecodeTab* tab_in, int exact_in,
-                       cudaStream_t st, const P2PArgs* x = nullptr, float* gstage = nullptr,
+                       cudaStream_t st, const P2PArgs* x = nullptr, const StageDst* gs = nullptr,
                        const P2PArgs* xs = nullptr, unsigned int* sched = nullptr, float fold_scale = 0.f,
-                       double* gnorm2 = nullptr) {
+                       double* gnorm2 = nullptr, double* const* gclear = nullptr) {
     if (L == nullptr) return fail(CDSGD_ERR_ARG, "layout is NULL");
     if (nr < 1 || nr > MAX_RANKS - 1) return fail(CDSGD_ERR_ARG, "nranks must be in [1, %d]", MAX_RANKS - 1);
     if ((gnext == nullptr) != (loc == nullptr)) return fail(CDSGD_ERR_ARG, "g_next and loc_out go together");
@@ -407,11 +432,13 @@ int launch_apply_quant(const cdsgd_layout* L, float* W, const uint32_t* gathered
     a.skip_below = skip_below;
     a.gnorm = gnorm;
     a.x = x != nullptr ? *x : P2PArgs{};
-    a.gstage = gstage;
+    a.gs = gs != nullptr ? *gs : StageDst{};
     a.xs = xs != nullptr ? *xs : P2PArgs{};
     a.sched = sched;
     a.fold_scale = fold_scale;
     a.gnorm2 = gnorm2;
+    a.gclear[0] = gclear != nullptr ? gclear[0] : nullptr;
+    a.gclear[1] = gclear != nullptr ? gclear[1] : nullptr;
     DecodeTab tab;
     int exact;
     if (tab_in != nullptr) {
@@ -425,12 +452,12 @@ int launch_apply_quant(const cdsgd_layout* L, float* W, const uint32_t* gathered
     const KeyTab kt = L->tab();
 #define AQ(R)                                                                                   \
     case R:                                                                                     \
-        k_apply_quant<R><<<tile_grid(k_apply_quant<R>, kt.ntiles), THREADS, 0, st>>>(a, kt, tab); \
+        launch_pdl(k_apply_quant<R>, tile_grid(k_apply_quant<R>, kt.ntiles), THREADS, 0, st, a, kt, tab); \
         break
     switch (nr) {
         AQ(1); AQ(2); AQ(3); AQ(4); AQ(5); AQ(6); AQ(7); AQ(8);
         default:
-            k_apply_quant<0><<<tile_grid(k_apply_quant<0>, kt.ntiles), THREADS, 0, st>>>(a, kt, tab);
+            launch_pdl(k_apply_quant<0>, tile_grid(k_apply_quant<0>, kt.ntiles), THREADS, 0, st, a, kt, tab);
     }
 #undef AQ
     LAUNCH_CHECK();
@@ -439,7 +466,7 @@ int launch_apply_quant(const cdsgd_layout* L, float* W, const uint32_t* gathered
 
 int launch_apply_full(float* W, const float* gsum, int nr, int64_t n, double eta_g, const float* gnext,
                       float* loc, double eta_l, const uint64_t* err, uint64_t skip_below, double* gnorm,
-                      cudaStream_t st) {
+                      cudaStream_t st, double* const* gclear = nullptr) {
     if (nr < 1) return fail(CDSGD_ERR_ARG, "nranks must be >= 1");
     if ((gnext == nullptr) != (loc == nullptr)) return fail(CDSGD_ERR_ARG, "g_next and loc_out go together");
     if (n == 0) return CDSGD_OK;
@@ -455,6 +482,8 @@ int launch_apply_full(float* W, const float* gsum, int nr, int64_t n, double eta
     a.err = err;
     a.skip_below = skip_below;
     a.gnorm = gnorm;
+    a.gclear[0] = gclear != nullptr ? gclear[0] : nullptr;
+    a.gclear[1] = gclear != nullptr ? gclear[1] : nullptr;
     const int rc = launch_af_tma_cfg(a, st);
     if (rc != CDSGD_OK) return rc;
     LAUNCH_CHECK();
@@ -466,9 +495,11 @@ int launch_fused_cfg(const FusedArgs& a, const KeyTab& kt, const DecodeTab& tab,
     // fewer than 2 whole-tile tasks per resident warp: split tiles into chunk tasks
     const int64_t warps = static_cast<int64_t>(resident_blocks(k_fused_ldg<NR, AP, CHUNKS>, THREADS)) * WARPS_PER_BLOCK;
     if (kt.ntiles < 2 * warps)
-        k_fused_ldg<NR, AP, 1><<<tile_grid(k_fused_ldg<NR, AP, 1>, kt.ntiles * CHUNKS), THREADS, 0, st>>>(a, kt, tab);
+        launch_pdl(k_fused_ldg<NR, AP, 1>, tile_grid(k_fused_ldg<NR, AP, 1>, kt.ntiles * CHUNKS), THREADS, 0, st, a, kt,
+                   tab);
     else
-        k_fused_ldg<NR, AP, CHUNKS><<<tile_grid(k_fused_ldg<NR, AP, CHUNKS>, kt.ntiles), THREADS, 0, st>>>(a, kt, tab);
+        launch_pdl(k_fused_ldg<NR, AP, CHUNKS>, tile_grid(k_fused_ldg<NR, AP, CHUNKS>, kt.ntiles), THREADS, 0, st, a, kt,
+                   tab);
     return CDSGD_OK;
 }
 int launch_fused(int nr, int apply, const FusedArgs& a, const KeyTab& kt, const DecodeTab& tab, cudaStream_t st) {
@@ -593,6 +624,11 @@ struct cdsgd_engine {
     bool xused[2] = {false, false};  // round parity p used the NCCL stream
     unsigned int* counters = nullptr;  // [4] grid-completion counters (K1/fused, K2, stage, reduce)
     // P2P correction rounds (sharded exact reduce over NVLink, no NCCL)
+    int64_t chunk = 0;  // elements per shard owner (P2P exact correction), a multiple of 4
+    // P2P exact staging: false = pull (my g_t stays local, owners load it over NVLink),
+    // true = push (K2 stores each element into its owner's receive row). Pull measured
+    // faster at N=4 (461 vs 442 Gelem/s): the pushes make K2 NVLink-bound. CDSGD_STAGE_PUSH=1.
+    bool stage_push = false;
     int64_t off_W = 0, off_stage[2] = {0, 0}, off_gready = 0, off_gfreed = 0, off_wdone = 0, off_gpart = 0;
     int64_t last_stage[2] = {-1, -1};  // last correction round that used staging slot s
     int64_t ncorr = 0;                 // P2P correction rounds staged so far (slot = ncorr & 1)
@@ -603,6 +639,8 @@ struct cdsgd_engine {
     bool fuse = false;                 // apply(t-1) + quantize(t) in one kernel (N=1 or P2P)
     bool pcorr = false;                // P2P mode: correction rounds by the exact sharded NVLink reduce
     bool diag_local_codes = false;     // timing diagnostic: store codes only locally
+    bool diag_no_wait = false;         // timing diagnostic: skip the code-exchange flag waits
+    int sc_fence = 0;                  // CDSGD_SC_FENCE=1: fence.sc.sys publish (A/B knob)
     // profiling: event pairs per kernel class (0 quant, 1 apply_q, 2 apply_f, 3 local, 4 exchange, 5 fused,
     // 6 stage, 7 reduce, 8 wait, 9 fused local-only)
     bool prof = false;
@@ -648,6 +686,18 @@ int round_compressed(const cdsgd_engine* E, int64_t t, bool* out) {
 
 int64_t words_of(const cdsgd_engine* E) { return E->L->nwords; }
 
+// Grad-norm ring: round p's slot. With >= 4 slots the kernel accumulating round p zeroes
+// the slots of the next two rounds in-kernel (pdl_enter), so no memset breaks the
+// programmatic-launch chain; a shorter ring falls back to a memset per round.
+double* gnorm_slot(const cdsgd_engine* E, int64_t p) {
+    return (E->d.gnorm_sq != nullptr && E->d.gnorm_ring > 0) ? E->d.gnorm_sq + (p % E->d.gnorm_ring) : nullptr;
+}
+bool gnorm_ahead(const cdsgd_engine* E) { return E->d.gnorm_sq != nullptr && E->d.gnorm_ring >= 4; }
+void gnorm_clears(const cdsgd_engine* E, int64_t first, double** clr) {
+    clr[0] = gnorm_ahead(E) ? gnorm_slot(E, first) : nullptr;
+    clr[1] = gnorm_ahead(E) ? gnorm_slot(E, first + 1) : nullptr;
+}
+
 // ---- P2P correction rounds (kernels_corr.cuh)
 template <typename T>
 T* at(char* base, int64_t off) { return reinterpret_cast<T*>(base + off); }
@@ -655,11 +705,19 @@ T* at(char* base, int64_t off) { return reinterpret_cast<T*>(base + off); }
 // Round t is a correction: g_t goes to staging slot ncorr & 1 where every rank can
 // read it. prepare_stage fills the destination + protocol and advances the state;
 // the copy is then either fused into K2 (which reads g_t anyway) or run by k_stage.
-void prepare_stage(cdsgd_engine* E, int64_t t, float** dst, P2PArgs* x) {
+void prepare_stage(cdsgd_engine* E, int64_t t, StageDst* dst, P2PArgs* x) {
     const int nr = E->d.nranks, me = E->d.rank;
     const int s = static_cast<int>(E->ncorr & 1);
     char* local = E->peer[me];
-    *dst = at<float>(local, E->off_stage[s]);
+    *dst = StageDst{};
+    if (E->stage_push) {
+        dst->chunk = E->chunk;
+        for (int o = 0; o < nr; ++o)  // owner o's receive row [me], indexed by element
+            dst->base[o] = at<float>(E->peer[o], E->off_stage[s]) + (static_cast<int64_t>(me) - o) * E->chunk;
+    } else {  // pull: g_t stays in my own stage; owners read it over NVLink
+        dst->chunk = std::max<int64_t>(E->L->n, TILE_ELEMS) + 4;
+        dst->base[0] = at<float>(local, E->off_stage[s]);
+    }
     *x = P2PArgs{};
     x->nranks = nr;
     for (int r = 0; r < nr; ++r) x->publish[r] = at<uint64_t>(E->peer[r], E->off_gready) + s * nr + me;
@@ -667,6 +725,7 @@ void prepare_stage(cdsgd_engine* E, int64_t t, float** dst, P2PArgs* x) {
     x->wait_value = E->last_stage[s] >= 0 ? static_cast<uint64_t>(E->last_stage[s]) + 1 : 0;
     x->publish_value = static_cast<uint64_t>(t) + 1;
     x->counter = E->counters + 2;
+    x->sc_fence = E->sc_fence;
     x->err = E->d.err;
     E->last_stage[s] = t;
     E->pend_slot = s;
@@ -677,9 +736,9 @@ int p2p_stage(cdsgd_engine* E, int64_t t, const float* g, cudaStream_t C) {
     StageArgs a{};
     a.g = g;
     a.n = E->L->n;
-    prepare_stage(E, t, &a.stage, &a.x);
+    prepare_stage(E, t, &a.gs, &a.x);
     const long pi = prof_start(E, 6, C);
-    k_stage<<<flat_grid(k_stage, (a.n + 3) / 4), THREADS, 0, C>>>(a);
+    launch_pdl(k_stage, flat_grid(k_stage, (a.n + 3) / 4), THREADS, 0, C, a);
     prof_stop(E, pi, C);
     LAUNCH_CHECK();
     return CDSGD_OK;
@@ -699,7 +758,7 @@ int reduce_ctas() {
 template <int NR>
 void launch_reduce_t(const ReduceArgs& a, int64_t len, cudaStream_t C) {
     const int grid = std::min(flat_grid(k_reduce<NR>, (len + 3) / 4), reduce_ctas());
-    k_reduce<NR><<<grid, THREADS, 0, C>>>(a);
+    launch_pdl(k_reduce<NR>, grid, THREADS, 0, C, a);
 }
 
 // Apply correction round p: reduce my shard from every rank's stage, broadcast W',
@@ -710,7 +769,8 @@ int p2p_reduce(cdsgd_engine* E, int64_t p, cudaStream_t C) {
     char* local = E->peer[me];
     ReduceArgs a{};
     for (int r = 0; r < nr; ++r) {
-        a.stage[r] = at<const float>(E->peer[r], E->off_stage[s]);
+        a.stage[r] = E->stage_push ? at<const float>(local, E->off_stage[s]) + static_cast<int64_t>(r) * E->chunk - E->s0
+                                   : at<const float>(E->peer[r], E->off_stage[s]);
         a.Wdst[r] = at<float>(E->peer[r], E->off_W);
         a.gpart_dst[r] = at<double>(E->peer[r], E->off_gpart) + s * nr + me;
         a.xa.publish[r] = at<uint64_t>(E->peer[r], E->off_gfreed) + s * nr + me;
@@ -728,10 +788,10 @@ int p2p_reduce(cdsgd_engine* E, int64_t p, cudaStream_t C) {
     a.xa.wait_value = static_cast<uint64_t>(p) + 1;
     a.xa.publish_value = static_cast<uint64_t>(p) + 1;
     a.xa.counter = E->counters + 3;
+    a.xa.sc_fence = E->sc_fence;
     a.xa.err = E->d.err;
     a.xb.nranks = nr;
     a.xb.publish_value = static_cast<uint64_t>(p) + 1;
-    CUDA_TRY(cudaMemsetAsync(E->gacc, 0, sizeof(double), C));
     const long pi = prof_start(E, 7, C);
     const int64_t len = E->s1 - E->s0;
     switch (nr) {
@@ -750,10 +810,12 @@ int p2p_reduce(cdsgd_engine* E, int64_t p, cudaStream_t C) {
     w.wait_flags = at<const uint64_t>(local, E->off_wdone);
     w.wait_value = static_cast<uint64_t>(p) + 1;
     w.err = E->d.err;
-    double* gn = (E->d.gnorm_sq != nullptr && E->d.gnorm_ring > 0) ? E->d.gnorm_sq + (p % E->d.gnorm_ring) : nullptr;
+    double* gn = gnorm_slot(E, p);
+    double* clr[2];
+    gnorm_clears(E, p + 1, clr);
     prof_stop(E, pi, C);
     const long pw = prof_start(E, 8, C);
-    k_wait_sum<<<1, 32, 0, C>>>(w, at<const double>(local, E->off_gpart) + s * nr, nr, gn);
+    launch_pdl(k_wait_sum, 1, 32, 0, C, w, at<const double>(local, E->off_gpart) + s * nr, nr, gn, clr[0], clr[1]);
     prof_stop(E, pw, C);
     LAUNCH_CHECK();
     return CDSGD_OK;
@@ -774,7 +836,7 @@ int p2p_reduce_async(cdsgd_engine* E, int64_t t, cudaStream_t C) {
 // Finish round p: wait for its exchange, then K2 (codes) or K3 (full) fused with
 // the local update from g_next (nullable).
 int engine_apply(cdsgd_engine* E, int64_t p, bool comp, const float* gp, const float* gnext, cudaStream_t C,
-                 float* gstage = nullptr, const P2PArgs* xs = nullptr, bool fold = false) {
+                 const StageDst* gs = nullptr, const P2PArgs* xs = nullptr, bool fold = false) {
     const int nr = E->d.nranks;
     if (!comp && E->p2p && E->pcorr) {  // P2P correction: exact sharded reduce, then (optionally) the local update
         int rc = CDSGD_OK;
@@ -788,11 +850,10 @@ int engine_apply(cdsgd_engine* E, int64_t p, bool comp, const float* gp, const f
     if (nr > 1 && E->xused[p & 1]) CUDA_TRY(cudaStreamWaitEvent(C, E->evX[p & 1], 0));
     const int64_t rel = p - E->err_base + 1;
     const uint64_t skip_below = rel <= 0 ? 0ull : (static_cast<uint64_t>(rel) << CDSGD_INDEX_BITS);
-    double* gn = nullptr;
-    if (E->d.gnorm_sq != nullptr && E->d.gnorm_ring > 0) {
-        gn = E->d.gnorm_sq + (p % E->d.gnorm_ring);
-        CUDA_TRY(cudaMemsetAsync(gn, 0, sizeof(double), C));
-    }
+    double* gn = gnorm_slot(E, p);
+    if (gn != nullptr && !gnorm_ahead(E)) CUDA_TRY(cudaMemsetAsync(gn, 0, sizeof(double), C));
+    double* clr[2];
+    gnorm_clears(E, p + (comp && fold ? 2 : 1), clr);
     float* loc = gnext ? E->d.loc : nullptr;
     if (comp) {
         P2PArgs x{};
@@ -806,26 +867,25 @@ int engine_apply(cdsgd_engine* E, int64_t p, bool comp, const float* gp, const f
             x.wait_value = static_cast<uint64_t>(p) + 1;
             x.publish_value = static_cast<uint64_t>(p) + 1;
             x.counter = E->counters + 1;
+            x.sc_fence = E->sc_fence;
             x.err = E->d.err;
+            if (E->diag_no_wait) x.wait_value = 0;
         }
-        double* gn2 = nullptr;  // grad-norm slot of the folded correction round p+1
-        if (fold && E->d.gnorm_sq != nullptr && E->d.gnorm_ring > 0) {
-            gn2 = E->d.gnorm_sq + ((p + 1) % E->d.gnorm_ring);
-            CUDA_TRY(cudaMemsetAsync(gn2, 0, sizeof(double), C));
-        }
+        double* gn2 = fold ? gnorm_slot(E, p + 1) : nullptr;  // grad-norm slot of the folded correction p+1
+        if (gn2 != nullptr && !gnorm_ahead(E)) CUDA_TRY(cudaMemsetAsync(gn2, 0, sizeof(double), C));
         const long pi = prof_start(E, 1, C);
         const int rc = launch_apply_quant(E->L, E->d.weights, E->d.gathered[p & 1], nr, words_of(E), E->d.alpha,
                                           E->d.eta_global, gnext, loc, E->d.eta_local, E->d.err, skip_below, gn,
-                                          &E->tab, E->exact, C, &x, gstage, xs,
+                                          &E->tab, E->exact, C, &x, gs, xs,
                                           E->sched != nullptr ? E->sched + 2 : nullptr,
-                                          fold ? static_cast<float>(E->d.eta_global) : 0.f, gn2);
+                                          fold ? static_cast<float>(E->d.eta_global) : 0.f, gn2, clr);
         prof_stop(E, pi, C);
         return rc;
     }
     const float* gsum = nr > 1 ? E->d.gsum[p & 1] : gp;
     const long pi = prof_start(E, 2, C);
     const int rc = launch_apply_full(E->d.weights, gsum, nr, E->L->n, E->d.eta_global, gnext, loc, E->d.eta_local,
-                                     E->d.err, skip_below, gn, C);
+                                     E->d.err, skip_below, gn, C, clr);
     prof_stop(E, pi, C);
     return rc;
 }
@@ -868,7 +928,9 @@ extern "C" int cdsgd_engine_create(const cdsgd_engine_desc* d, const cdsgd_layou
         }
     }
     cudaError_t e = cudaSuccess;
-    if (d->nranks > 1) {
+    if (d->gnorm_sq != nullptr && d->gnorm_ring > 0)  // slots are zeroed ahead in-kernel from here on
+        e = cudaMemset(d->gnorm_sq, 0, static_cast<size_t>(d->gnorm_ring) * sizeof(double));
+    if (d->nranks > 1 && e == cudaSuccess) {
         int lo = 0, hi = 0;
         cudaDeviceGetStreamPriorityRange(&lo, &hi);
         e = cudaStreamCreateWithPriority(&E->xs, cudaStreamNonBlocking, hi);
@@ -887,18 +949,21 @@ extern "C" int cdsgd_engine_create(const cdsgd_engine_desc* d, const cdsgd_layou
 
 namespace {
 int64_t align256(int64_t v) { return (v + 255) & ~int64_t(255); }
+// Shard owned by each rank in the P2P exact correction: ceil(n/N) rounded up to 4 elements.
+int64_t p2p_chunk(int32_t nranks, int64_t n) { return (((n + nranks - 1) / nranks) + 3) / 4 * 4; }
 // Symmetric buffer: codes slot 0 | slot 1 | ready[2][N] | freed[2][N] | W [n] |
-// stage 0 [n] | stage 1 [n] | gready[2][N] | gfreed[2][N] | wdone[N] | gpart[2][N] | end
+// recv 0 [N][chunk] | recv 1 [N][chunk] | gready[2][N] | gfreed[2][N] | wdone[N] | gpart[2][N] | end
 void p2p_offsets(int32_t nranks, int64_t n, int64_t words, int64_t* off /* [12] */) {
     const int64_t flags = align256(2 * nranks * 8);
+    const int64_t recv = align256(4 * static_cast<int64_t>(nranks) * p2p_chunk(nranks, n));
     off[0] = 0;
     off[1] = align256(static_cast<int64_t>(nranks) * words * 4);
     off[2] = 2 * off[1];
     off[3] = off[2] + flags;
     off[4] = off[3] + flags;
     off[5] = off[4] + align256(4 * n);
-    off[6] = off[5] + align256(4 * n);
-    off[7] = off[6] + align256(4 * n);
+    off[6] = off[5] + recv;
+    off[7] = off[6] + recv;
     off[8] = off[7] + flags;
     off[9] = off[8] + flags;
     off[10] = off[9] + align256(nranks * 8);
@@ -951,19 +1016,29 @@ extern "C" int cdsgd_engine_attach_p2p(cdsgd_engine* E, void* const* peer_bases,
         CUDA_TRY(cudaMemcpy(wsym, E->d.weights, 4 * E->L->n, cudaMemcpyDeviceToDevice));
         E->d.weights = wsym;
     }
-    const int64_t chunk = (((E->L->n + nranks - 1) / nranks) + 3) / 4 * 4;
+    const int64_t chunk = p2p_chunk(nranks, E->L->n);
+    E->chunk = chunk;
     E->s0 = std::min<int64_t>(E->L->n, chunk * E->d.rank);
     E->s1 = std::min<int64_t>(E->L->n, E->s0 + chunk);
     if (E->counters == nullptr) {
         CUDA_TRY(cudaMalloc(&E->counters, 4 * sizeof(unsigned int)));
         CUDA_TRY(cudaMemset(E->counters, 0, 4 * sizeof(unsigned int)));
     }
-    if (E->gacc == nullptr) CUDA_TRY(cudaMalloc(&E->gacc, sizeof(double)));
+    if (E->gacc == nullptr) {
+        CUDA_TRY(cudaMalloc(&E->gacc, sizeof(double)));
+        CUDA_TRY(cudaMemset(E->gacc, 0, sizeof(double)));
+    }
     E->p2p = true;
     E->pcorr = exact_correction != 0;
     {
         const char* nr = getenv("CDSGD_DIAG_NO_REMOTE_CODES");  // timing diagnostic only: wrong results
         E->diag_local_codes = nr != nullptr && nr[0] == '1';
+        const char* nw = getenv("CDSGD_DIAG_NO_WAIT");  // timing diagnostic only: races, wrong results
+        E->diag_no_wait = nw != nullptr && nw[0] == '1';
+        const char* sp = getenv("CDSGD_STAGE_PUSH");
+        E->stage_push = sp != nullptr && sp[0] == '1';
+        const char* sf = getenv("CDSGD_SC_FENCE");
+        E->sc_fence = sf != nullptr && sf[0] == '1';
     }
     {
         const char* nf = getenv("CDSGD_NO_FUSE");
@@ -1058,6 +1133,8 @@ extern "C" int cdsgd_engine_step(cdsgd_engine* E, const float* g, void* stream) 
             x.wait_value = E->last_use[p] >= 0 ? static_cast<uint64_t>(E->last_use[p]) + 1 : 0;
             x.publish_value = static_cast<uint64_t>(t) + 1;
             x.counter = E->counters;
+            x.sc_fence = E->sc_fence;
+            if (E->diag_no_wait) x.wait_value = 0;
             x.err = E->d.err;
             const uint64_t tag = static_cast<uint64_t>(t - E->err_base) << CDSGD_INDEX_BITS;
             const long pi = prof_start(E, 0, C);
@@ -1115,9 +1192,10 @@ extern "C" int cdsgd_engine_step(cdsgd_engine* E, const float* g, void* stream) 
         a.skip_below = rel <= 0 ? 0ull : (static_cast<uint64_t>(rel) << CDSGD_INDEX_BITS);
         a.err = E->d.err;
         a.sched = E->sched;
-        if (has_pend && E->d.gnorm_sq != nullptr && E->d.gnorm_ring > 0) {
-            a.gnorm = E->d.gnorm_sq + (pnd % E->d.gnorm_ring);
-            CUDA_TRY(cudaMemsetAsync(a.gnorm, 0, sizeof(double), C));
+        if (has_pend) {
+            a.gnorm = gnorm_slot(E, pnd);
+            if (a.gnorm != nullptr && !gnorm_ahead(E)) CUDA_TRY(cudaMemsetAsync(a.gnorm, 0, sizeof(double), C));
+            gnorm_clears(E, pnd + 1, a.gclear);
         }
         if (!has_pend) a.skip_below = 0;
         if (E->p2p) {
@@ -1134,17 +1212,21 @@ extern "C" int cdsgd_engine_step(cdsgd_engine* E, const float* g, void* stream) 
             a.xq.wait_value = E->last_use[p] >= 0 ? static_cast<uint64_t>(E->last_use[p]) + 1 : 0;
             a.xq.publish_value = static_cast<uint64_t>(t) + 1;
             a.xq.counter = E->counters;
+            a.xq.sc_fence = E->sc_fence;
             a.xq.err = E->d.err;
             a.xa.wait_flags = reinterpret_cast<const uint64_t*>(local + E->off_ready) + q * nr;
             a.xa.wait_value = static_cast<uint64_t>(pnd) + 1;
             a.xa.publish_value = static_cast<uint64_t>(pnd) + 1;
             a.xa.counter = E->counters;
+            a.xa.sc_fence = E->sc_fence;
             a.xa.err = E->d.err;
+            if (E->diag_no_wait) a.xq.wait_value = a.xa.wait_value = 0;
             E->last_use[p] = t;
         }
         E->rlog.push_back(static_cast<int8_t>(E->rcur));
         const long pi = prof_start(E, has_pend ? 5 : 9, C);
-        rc = launch_fused(nr, !has_pend ? APPLY_L : (E->pend_comp ? APPLY_Q : APPLY_F), a, E->L->tab(), E->tab, C);
+        const int ap = !has_pend ? APPLY_L : (E->pend_comp ? APPLY_Q : APPLY_F);
+        rc = launch_fused(nr, ap, a, E->L->tab(), E->tab, C);
         prof_stop(E, pi, C);
         if (rc != CDSGD_OK) return rc;
         E->rcur ^= 1;
@@ -1176,6 +1258,8 @@ extern "C" int cdsgd_engine_step(cdsgd_engine* E, const float* g, void* stream) 
             x.wait_value = E->last_use[p] >= 0 ? static_cast<uint64_t>(E->last_use[p]) + 1 : 0;
             x.publish_value = static_cast<uint64_t>(t) + 1;
             x.counter = E->counters;
+            x.sc_fence = E->sc_fence;
+            if (E->diag_no_wait) x.wait_value = 0;
             x.err = E->d.err;
             rc = launch_quant_tma_cfg(g, E->d.residual[E->rcur], E->d.residual[E->rcur ^ 1], mine, E->L->tab(),
                                       E->d.alpha, E->d.err, tag, C, x);
@@ -1223,10 +1307,10 @@ extern "C" int cdsgd_engine_step(cdsgd_engine* E, const float* g, void* stream) 
         bool staged = false;
         if (E->pending && !comp && E->p2p && E->pcorr && E->pend_comp) {
             // correction round after a compressed one: K2(t-1) also writes g_t to the stage
-            float* dst = nullptr;
+            StageDst dst{};
             P2PArgs xs{};
             prepare_stage(E, t, &dst, &xs);
-            rc = engine_apply(E, E->pend_t, E->pend_comp, E->pend_grad, g, C, dst, &xs);
+            rc = engine_apply(E, E->pend_t, E->pend_comp, E->pend_grad, g, C, &dst, &xs);
             staged = true;
         } else if (E->pending && !comp && nr == 1 && E->pend_comp && E->fuse) {
             // N=1: this correction round's mean is g_t itself -> apply it in the same pass

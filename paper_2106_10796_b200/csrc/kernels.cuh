@@ -150,12 +150,38 @@ struct P2PArgs {
     unsigned int* counter;              // local grid-completion counter (0 between launches)
     uint64_t* err;                      // err[1] receives EXCHANGE_TIMEOUT
     int nranks;                         // 0: exchange disabled
+    int sc_fence;                       // A/B knob: fence.sc.sys + relaxed counter instead of acq_rel
 };
+
+// Programmatic dependent launch (engine kernels are launched with programmatic stream
+// serialization): a kernel may become resident while its stream predecessor drains, so
+// every engine kernel calls pdl_wait() before its first memory access (a no-op without
+// the attribute), then pdl_trigger() so its own successor's launch overlaps its body.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+// Grad-norm ring: the kernel accumulating round p zeroes the slots of rounds p+1 and p+2
+// (two ahead covers the N=1 fold, which accumulates two rounds); stream order makes this
+// race-free and removes a memset (and a PDL break) per round.
+__device__ __forceinline__ void pdl_enter(double* clear0, double* clear1) {
+    pdl_wait();
+    pdl_trigger();
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        if (clear0 != nullptr) *clear0 = 0.0;
+        if (clear1 != nullptr) *clear1 = 0.0;
+    }
+}
 
 __device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* p) {
     uint64_t v;
     asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
     return v;
+}
+// Release pattern for a batch of flags: ONE system-scope fence, then relaxed strong
+// stores. (A st.release.sys per flag costs a fence each: 8 of them in the last CTA of a
+// fused launch at N=4 measured ~13 us.)
+__device__ __forceinline__ void fence_acq_rel_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
+__device__ __forceinline__ void st_relaxed_sys(uint64_t* p, uint64_t v) {
+    asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 __device__ __forceinline__ void st_release_sys(uint64_t* p, uint64_t v) {
     asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
@@ -180,18 +206,39 @@ __device__ __forceinline__ void p2p_wait(const P2PArgs& x) {
     }
 }
 
+__device__ __forceinline__ unsigned atom_add_acq_rel_sys(unsigned int* p, unsigned v) {
+    unsigned old;
+    asm volatile("atom.acq_rel.sys.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+    return old;
+}
+// Thread 0 of each CTA, after a __syncthreads: count the CTA in on the grid-completion
+// counter; true for the last CTA. The acq_rel system-scope atomic releases every write
+// of the CTA (cumulative through the barrier), remote NVLink stores included, and the
+// last CTA's atomic acquires all of them, so its st.release.sys flags publish the whole
+// grid's output. (A full fence.sc.sys per CTA measured ~15 us slower per launch at N=4.)
+__device__ __forceinline__ bool grid_arrive_last(unsigned int* counter, bool sc_fence) {
+    unsigned prev;
+    if (sc_fence) {
+        __threadfence_system();
+        prev = atomicAdd(counter, 1u);
+        if (prev == gridDim.x - 1) __threadfence_system();
+    } else {
+        prev = atom_add_acq_rel_sys(counter, 1u);
+    }
+    if (prev != gridDim.x - 1) return false;
+    *counter = 0u;  // ready for the next launch (stream-ordered)
+    return true;
+}
+
 // Block-wide epilogue: the last CTA to finish publishes publish_value to every peer.
 __device__ __forceinline__ void p2p_publish(const P2PArgs& x) {
     if (x.nranks <= 0) return;
     __syncthreads();
     if (threadIdx.x == 0) {
-        __threadfence_system();
-        const unsigned prev = atomicAdd(x.counter, 1u);
-        if (prev == gridDim.x - 1) {
-            __threadfence_system();
-            *x.counter = 0u;
+        if (grid_arrive_last(x.counter, x.sc_fence != 0)) {
+            fence_acq_rel_sys();
             for (int r = 0; r < x.nranks; ++r)
-                if (x.publish[r] != nullptr) st_release_sys(x.publish[r], x.publish_value);
+                if (x.publish[r] != nullptr) st_relaxed_sys(x.publish[r], x.publish_value);
         }
     }
 }
@@ -221,15 +268,12 @@ __device__ __forceinline__ void p2p_publish2(const P2PArgs& a, const P2PArgs& b,
     if (a.nranks <= 0 && b.nranks <= 0) return;
     __syncthreads();
     if (threadIdx.x == 0) {
-        __threadfence_system();
-        const unsigned prev = atomicAdd(counter, 1u);
-        if (prev == gridDim.x - 1) {
-            __threadfence_system();
-            *counter = 0u;
+        if (grid_arrive_last(counter, (a.nranks > 0 ? a.sc_fence : b.sc_fence) != 0)) {
             const P2PArgs* xs[2] = {&a, &b};
+            fence_acq_rel_sys();
             for (int i = 0; i < 2; ++i)
                 for (int r = 0; r < xs[i]->nranks; ++r)
-                    if (xs[i]->publish[r] != nullptr) st_release_sys(xs[i]->publish[r], xs[i]->publish_value);
+                    if (xs[i]->publish[r] != nullptr) st_relaxed_sys(xs[i]->publish[r], xs[i]->publish_value);
         }
     }
 }
@@ -311,6 +355,21 @@ __device__ __forceinline__ double decode1(uint32_t code, double alpha) {
     return code == 1u ? alpha : (code == 2u ? -alpha : 0.0);
 }
 
+// Scatter of a correction round's gradient to the element owners (P2P exact mode):
+// element e, owned by rank o = e / chunk, lands at base[o] + e, where base[o] is owner o's
+// receive row for this rank shifted by -o*chunk. Each owner then reduces its shard from
+// LOCAL memory (the NVLink transfer is fire-and-forget stores issued while the gradient
+// streams through the kernel anyway, instead of latency-bound remote loads).
+struct StageDst {
+    float* base[MAX_RANKS_P2P];
+    int64_t chunk;  // elements per owner, a multiple of 4; 0 = no staging
+};
+// Owner row of element e given the owner o0 of the tile start and the next boundary bnd.
+__device__ __forceinline__ float* stage_at(const StageDst& s, int64_t e, int o0, int64_t bnd) {
+    const int o = s.chunk >= TILE_ELEMS ? o0 + (e >= bnd ? 1 : 0) : static_cast<int>(e / s.chunk);
+    return s.base[o] + e;
+}
+
 // ================================================================ K2: apply_quant
 // Fused: decode N gathered payloads, ascending-rank fp64 sum / N (engine.py:249-255),
 // W' = W - eta_g*mean (engine.py:511) on fp32 W, loc = W' - eta_l*g_next (Eq. 11,
@@ -329,7 +388,7 @@ struct ApplyQArgs {
     uint64_t skip_below;
     double* gnorm;
     P2PArgs x;      // fused exchange: wait for peers' codes, then release the slot
-    float* gstage;  // non-null: also copy g_next here (staging of a P2P correction round)
+    StageDst gs;    // chunk != 0: also scatter g_next to the element owners (P2P correction round)
     P2PArgs xs;     // staging protocol: wait gfreed, publish gready
     unsigned int* sched;  // [2] dynamic tile scheduler {next tile, CTAs done}; nullptr = static ranges
     // N=1, the round after this one is a correction whose mean is g_next itself: also apply
@@ -337,6 +396,7 @@ struct ApplyQArgs {
     // with its grad-norm into gnorm2. 0 = off.
     float fold_scale;
     double* gnorm2;
+    double* gclear[2];  // grad-norm ring slots to zero (see pdl_enter), nullable
 };
 
 __device__ __forceinline__ double apply_mean_general(const uint32_t* codes, int nr, double alpha,
@@ -353,6 +413,7 @@ __device__ __forceinline__ double apply_mean_general(const uint32_t* codes, int 
 
 template <int NR>  // NR > 0: compile-time rank count; NR == 0: runtime (generic)
 __global__ void __launch_bounds__(256) k_apply_quant(ApplyQArgs a, KeyTab kt, DecodeTab tab) {
+    pdl_enter(a.gclear[0], a.gclear[1]);
     p2p_wait2(a.x, a.xs);
     const bool skip = a.err != nullptr && *reinterpret_cast<volatile uint64_t*>(a.err) < a.skip_below;
     __shared__ double s_mean[2 * MAX_RANKS + 1];
@@ -403,6 +464,12 @@ __global__ void __launch_bounds__(256) k_apply_quant(ApplyQArgs a, KeyTab kt, De
             const int nw = nw64 < TILE_WORDS ? static_cast<int>(nw64) : TILE_WORDS;
             const bool fast = NR > 0 && a.exact && ne == TILE_ELEMS && aligned_to(a.W + e0, 16) &&
                               (!do_loc || (aligned_to(a.gnext + e0, 16) && aligned_to(a.loc + e0, 16)));
+            int so0 = 0;
+            int64_t sbnd = 0;
+            if (a.gs.chunk != 0) {
+                so0 = static_cast<int>(e0 / a.gs.chunk);
+                sbnd = (so0 + 1) * a.gs.chunk;
+            }
             if (fast) {
                 constexpr int R = NR > 0 ? NR : 1;
                 uint32_t wv[R];
@@ -446,7 +513,7 @@ __global__ void __launch_bounds__(256) k_apply_quant(ApplyQArgs a, KeyTab kt, De
                     }
                     st_stream(a.W + e, w4[0], w4[1], w4[2], w4[3]);
                     if (do_loc) st_stream(a.loc + e, l4[0], l4[1], l4[2], l4[3]);
-                    if (a.gstage != nullptr) st_stream(a.gstage + e, g4[0], g4[1], g4[2], g4[3]);
+                    if (a.gs.chunk != 0) st_stream(stage_at(a.gs, e, so0, sbnd), g4[0], g4[1], g4[2], g4[3]);
                 }
             } else {
                 // generic path: lane l owns element 32s + l; word (2s + l/16), code l%16
@@ -484,7 +551,7 @@ __global__ void __launch_bounds__(256) k_apply_quant(ApplyQArgs a, KeyTab kt, De
                             gsq2 = __fma_rn(static_cast<double>(gn), static_cast<double>(gn), gsq2);
                         }
                         a.W[e] = wn;
-                        if (a.gstage != nullptr) a.gstage[e] = a.gnext[e];
+                        if (a.gs.chunk != 0) *stage_at(a.gs, e, so0, sbnd) = a.gnext[e];
                         if (a.gnorm != nullptr) gsq = __fma_rn(mean, mean, gsq);
                         if (rsv) bad_idx = static_cast<uint64_t>(e) < bad_idx ? static_cast<uint64_t>(e) : bad_idx;
                     }
@@ -619,6 +686,7 @@ struct ApplyFArgs {
     const uint64_t* err;
     uint64_t skip_below;
     double* gnorm;
+    double* gclear[2];
 };
 
 // engine.global_update / local_update with fp64 math (exact reference arithmetic
@@ -637,6 +705,7 @@ __global__ void k_global_update(TW* __restrict__ w, const TM* __restrict__ mean,
 template <typename TB, typename TG, typename TO>
 __global__ void k_local_update(const TB* __restrict__ base, const TG* __restrict__ g, TO* __restrict__ out,
                                int64_t n, double eta_l) {
+    pdl_enter(nullptr, nullptr);
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
         out[i] = from_d<TO>(__dsub_rn(to_d(base[i]), __dmul_rn(eta_l, to_d(g[i]))));
 }

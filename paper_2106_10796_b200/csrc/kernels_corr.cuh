@@ -3,18 +3,20 @@
 // Reference semantics (engine.py:252, 255, 511): the k-th round pushes full-precision
 // gradients, the server sums them in ascending worker id in fp64, divides by N and
 // applies W -= eta * mean. Here, with every rank holding a W replica in symmetric
-// memory:
-//   k_stage   (round t)   g_t -> my staging slot; release gready[slot][me] = t+1
-//   k_reduce  (round t+1) for MY shard of elements: acquire all gready, read every
-//             rank's staged g over NVLink, fp64 ascending-rank sum, / N (the
-//             reference's arithmetic), W' = W - eta*mean rounded once to fp32, store
-//             W' into EVERY rank's W replica (NVLink stores); publish gfreed (done
-//             reading the stages), the shard's sum(mean^2) and wdone[me] = t+1
+// memory and owning one shard [o*chunk, (o+1)*chunk) of the elements:
+//   stage     (round t)   g_t -> my staging slot (pull, default), or each element into its
+//             OWNER's receive row [my rank] (push: NVLink stores); fused into K2, which
+//             streams g_t anyway, or k_stage; release gready[slot][me] = t+1 everywhere
+//   k_reduce  (round t+1) for MY shard: acquire all gready, read the N ranks' values
+//             (pull: remote loads; push: local rows), fp64 ascending-rank sum, / N (the
+//             reference's arithmetic), W' = W - eta*mean rounded once to fp32, store W'
+//             into EVERY rank's W replica (NVLink stores); publish gfreed (stages
+//             reusable), the shard's sum(mean^2) and wdone[me] = t+1
 //   k_wait_sum            acquire all wdone (W' complete everywhere), grad-norm total
 // Per rank this moves 2(N-1)/N * 4n bytes each way over NVLink (a ring all-reduce's
-// volume) but nothing through intermediate HBM FIFOs and no NCCL kernels. The sum
-// is bitwise the reference's, and W replicas stay identical because each shard's
-// W' is computed once and broadcast.
+// volume) but nothing through intermediate HBM FIFOs and no NCCL kernels. The sum is
+// bitwise the reference's, and W replicas stay identical because each shard's W' is
+// computed once and broadcast.
 #pragma once
 #include "kernels.cuh"
 
@@ -22,38 +24,39 @@ namespace cdsgd {
 
 struct StageArgs {
     const float* g;
-    float* stage;
+    StageDst gs;  // owners' receive rows (kernels.cuh)
     int64_t n;
     P2PArgs x;  // wait: gfreed[slot][*] (previous use released); publish: gready[slot][me]
 };
 
 __global__ void __launch_bounds__(256) k_stage(StageArgs a) {
+    pdl_enter(nullptr, nullptr);
     p2p_wait(a.x);
     const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const int64_t nth = (int64_t)gridDim.x * blockDim.x;
-    const bool vec = aligned_to(a.g, 16) && aligned_to(a.stage, 16);
+    const bool vec = aligned_to(a.g, 16);
     int64_t done = 0;
-    if (vec) {
+    if (vec) {  // chunk is a multiple of 4: a float4 never straddles two owners
         const int64_t nv = a.n / 4;
         for (int64_t i = tid; i < nv; i += nth) {
             const float4 v = ld_stream(a.g + 4 * i);
-            st_stream(a.stage + 4 * i, v.x, v.y, v.z, v.w);
+            st_stream(a.gs.base[(4 * i) / a.gs.chunk] + 4 * i, v.x, v.y, v.z, v.w);
         }
         done = nv * 4;
     }
-    for (int64_t i = done + tid; i < a.n; i += nth) a.stage[i] = a.g[i];
+    for (int64_t i = done + tid; i < a.n; i += nth) a.gs.base[i / a.gs.chunk][i] = a.g[i];
     p2p_publish(a.x);
 }
 
 struct ReduceArgs {
-    const float* stage[MAX_RANKS_P2P];  // rank r's staging slot (mapped)
+    const float* stage[MAX_RANKS_P2P];  // rank r's staged g, indexed by element (mapped or local row)
     float* Wdst[MAX_RANKS_P2P];         // rank r's W replica (mapped)
     const float* W;                     // my W replica (read)
     int64_t s0, s1;                     // my shard [s0, s1)
     int nranks;
     double eta_g;
     double inv_n;                       // 1/N when N is a power of two, else 0 (divide)
-    double* gacc;                       // local accumulator of sum(mean^2) (zeroed by the host)
+    double* gacc;                       // local accumulator of sum(mean^2) (0 between launches)
     double* gpart_dst[MAX_RANKS_P2P];   // rank r's gpart[me]
     P2PArgs xa;                         // wait: gready[slot][*] >= t+1; publish: gfreed[slot][me]
     P2PArgs xb;                         // publish: wdone[me]
@@ -71,6 +74,7 @@ __device__ __forceinline__ float reduce_apply1(const float (&g)[NR], float w, do
 
 template <int NR>
 __global__ void __launch_bounds__(256) k_reduce(ReduceArgs a) {
+    pdl_enter(nullptr, nullptr);
     p2p_wait(a.xa);
     const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const int64_t nth = (int64_t)gridDim.x * blockDim.x;
@@ -92,7 +96,7 @@ __global__ void __launch_bounds__(256) k_reduce(ReduceArgs a) {
             for (int u = 0; u < U; ++u) {
                 const int64_t e = a.s0 + 4 * (i + u * nth);
 #pragma unroll
-                for (int r = 0; r < NR; ++r) gv[u][r] = *reinterpret_cast<const float4*>(a.stage[r] + e);  // NVLink
+                for (int r = 0; r < NR; ++r) gv[u][r] = ld_stream(a.stage[r] + e);  // pull: NVLink loads
                 wv[u] = ld_stream(a.W + e);
             }
 #pragma unroll
@@ -116,7 +120,7 @@ __global__ void __launch_bounds__(256) k_reduce(ReduceArgs a) {
             const int64_t e = a.s0 + 4 * i;
             float4 gv[NR];
 #pragma unroll
-            for (int r = 0; r < NR; ++r) gv[r] = *reinterpret_cast<const float4*>(a.stage[r] + e);
+            for (int r = 0; r < NR; ++r) gv[r] = ld_stream(a.stage[r] + e);
             const float4 wv = ld_stream(a.W + e);
             float g0[NR], g1[NR], g2[NR], g3[NR];
 #pragma unroll
@@ -146,17 +150,14 @@ __global__ void __launch_bounds__(256) k_reduce(ReduceArgs a) {
     // last CTA: broadcast the shard's sum(mean^2), then release gfreed and wdone
     __syncthreads();
     if (threadIdx.x == 0) {
-        __threadfence_system();
-        const unsigned prev = atomicAdd(a.xa.counter, 1u);
-        if (prev == gridDim.x - 1) {
-            __threadfence_system();
-            *a.xa.counter = 0u;
+        if (grid_arrive_last(a.xa.counter, a.xa.sc_fence != 0)) {
             const double total = *reinterpret_cast<volatile double*>(a.gacc);
+            *reinterpret_cast<volatile double*>(a.gacc) = 0.0;  // ready for the next correction round
             for (int r = 0; r < a.nranks; ++r) *reinterpret_cast<volatile double*>(a.gpart_dst[r]) = total;
-            __threadfence_system();
+            fence_acq_rel_sys();  // orders the gpart stores too
             for (int r = 0; r < a.nranks; ++r) {
-                if (a.xa.publish[r] != nullptr) st_release_sys(a.xa.publish[r], a.xa.publish_value);
-                if (a.xb.publish[r] != nullptr) st_release_sys(a.xb.publish[r], a.xb.publish_value);
+                if (a.xa.publish[r] != nullptr) st_relaxed_sys(a.xa.publish[r], a.xa.publish_value);
+                if (a.xb.publish[r] != nullptr) st_relaxed_sys(a.xb.publish[r], a.xb.publish_value);
             }
         }
     }
@@ -164,7 +165,8 @@ __global__ void __launch_bounds__(256) k_reduce(ReduceArgs a) {
 
 // One thread: acquire flags (W' shards of every rank have landed), then optionally
 // total the per-shard sum(mean^2) into the round's grad-norm slot.
-__global__ void k_wait_sum(P2PArgs x, const double* gpart, int n, double* out) {
+__global__ void k_wait_sum(P2PArgs x, const double* gpart, int n, double* out, double* clear0, double* clear1) {
+    pdl_enter(clear0, clear1);
     p2p_wait(x);
     if (threadIdx.x == 0 && out != nullptr) {
         double s = 0.0;

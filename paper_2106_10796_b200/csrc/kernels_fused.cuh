@@ -43,6 +43,7 @@ struct FusedArgs {
     P2PArgs xq;  // exchange of round t's codes (wait: slot freed; publish: ready)
     P2PArgs xa;  // exchange of round t-1's codes (wait: ready; publish: freed)
     unsigned int* sched;  // [2] dynamic tile scheduler {next tile, CTAs done}; nullptr = static ranges
+    double* gclear[2];    // grad-norm ring slots to zero (see pdl_enter), nullable
 };
 
 // Data moved with 128/256-bit coalesced loads straight into registers (all loads of a
@@ -53,6 +54,7 @@ template <int NR, int APPLY, int CH = CHUNKS>
 __global__ void __launch_bounds__(256, 2) k_fused_ldg(FusedArgs a, KeyTab kt, DecodeTab tab) {
     constexpr int SPL = CHUNKS / CH;  // tasks per tile
     __shared__ float s_upd[2 * MAX_RANKS + 1];
+    pdl_enter(a.gclear[0], a.gclear[1]);
     p2p_wait2(a.xq, a.xa);
     const uint64_t e0v = a.err != nullptr ? *reinterpret_cast<volatile uint64_t*>(a.err) : ~0ull;
     const bool q_off = e0v != NO_ERR;
@@ -268,7 +270,8 @@ __global__ void __launch_bounds__(256, 2) k_fused_ldg(FusedArgs a, KeyTab kt, De
             const bool mine_word = !fast || ((lane >> 3) >= c0 && (lane >> 3) < c0 + CH);
             if (lane < nw && !q_off && mine_word) {
                 if (a.xq.nranks > 0) {
-                    for (int r = 0; r < a.xq.nranks; ++r) a.xq.dst[r][w0 + lane] = myword;
+                    for (int r = 0; r < a.xq.nranks; ++r)
+                        if (a.xq.dst[r] != nullptr) a.xq.dst[r][w0 + lane] = myword;
                 } else {
                     a.words[w0 + lane] = myword;
                 }

@@ -106,6 +106,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
                    KeyTab kt, double alpha, uint64_t* err, uint64_t tag, P2PArgs x) {
     using SM = QuantSmem<G, WARPS, S>;
     extern __shared__ __align__(128) unsigned char smem[];
+    pdl_enter(nullptr, nullptr);
     p2p_wait(x);  // fused exchange: peers have released the slot we are about to fill
     const bool aborted = err != nullptr && *reinterpret_cast<volatile uint64_t*>(err) != NO_ERR;
     const int warp = threadIdx.x >> 5;
@@ -252,6 +253,7 @@ template <int WARPS, int S>
 __global__ void __launch_bounds__(WARPS * 32, 1) k_apply_full_tma(ApplyFArgs a) {
     using SM = ApplyFSmem<WARPS, S>;
     extern __shared__ __align__(128) unsigned char smem[];
+    pdl_enter(a.gclear[0], a.gclear[1]);
     if (a.err != nullptr && *reinterpret_cast<volatile const uint64_t*>(a.err) < a.skip_below) return;
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;

@@ -199,7 +199,7 @@ class CDSGDWorker:
         return out
 
     def grad_norm(self, t: int) -> float:
-        """||round-t mean gradient||_2 (engine.py:521); valid for the last gnorm_ring rounds."""
+        """||round-t mean gradient||_2 (engine.py:521); valid for the last gnorm_ring - 2 rounds."""
         if not self.gnorm_ring:
             raise ConfigError("grad-norm metric disabled (gnorm_ring=0)")
         return float(self.gnorm[t % self.gnorm_ring].sqrt().item())

@@ -1,11 +1,12 @@
 #!/bin/bash
-# N-GPU bench under env variants: bash mgpu_env_sweep.sh N "ENV=.." ...
+# N-GPU bench under env variants: bash mgpu_env_sweep.sh N "ENV=..[|bench args]" ...
 mkdir -p gpurun_out
 N=$1; shift
 i=0
 for v in "$@"; do
   i=$((i+1))
-  env $v timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 --master-port 29549 bench.py --gpus $N --steps 40 --warmup 10 --no-e2e $EXTRA > gpurun_out/mes_$i.log 2>&1
+  envp="${v%%|*}"; argp=""; [[ "$v" == *"|"* ]] && argp="${v#*|}"
+  env $envp timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 --master-port 29549 bench.py --gpus $N --steps 40 --warmup 10 --no-e2e $EXTRA $argp > gpurun_out/mes_$i.log 2>&1
   python - $i "$v" <<'PY'
 import json,sys
 f=f"gpurun_out/mes_{sys.argv[1]}.log"

@@ -79,6 +79,28 @@ def test_engine_n1_matches_oracle(pkg, case):
         assert abs(wk.grad_norm(t) - orc.grad_norms[t]) <= 1e-6 * max(1.0, orc.grad_norms[t])
 
 
+@pytest.mark.parametrize("ring", [2, 4])
+@pytest.mark.parametrize("sizes,k,warm", [([5000, 33], 4, 0), ([5000, 33], 3, 2), ([300_000], 2, 1)])
+def test_engine_grad_norm_ring(pkg, ring, sizes, k, warm):
+    # ring >= 4: the accumulating kernel zeroes the next two slots in-kernel (incl. the N=1
+    # fold, which accumulates two rounds); ring < 4: a memset per round
+    _, E, L, Wk = pkg
+    layout = L.Layout.from_lengths(sizes)
+    n = layout.total
+    hp = E.HyperParams(algo="cdsgd", workers=1, eta_global=0.1, eta_local=0.4, k=k, alpha=0.5, warmup_n=warm)
+    w0 = O.synthetic_weights(5, n)
+    wk = Wk.CDSGDWorker(layout, hp, w0, gnorm_ring=ring)
+    orc = O.LockstepOracle(w0.astype(np.float64), sizes, O.OracleHP("cdsgd", 1, 0.1, 0.4, k, 0.5, warm))
+    for t in range(14):
+        g = O.synthetic_grad(5, t, 0, n)
+        wk.step(torch.from_numpy(g).cuda())
+        orc.step([g])
+        if t >= 1:
+            assert abs(wk.grad_norm(t - 1) - orc.grad_norms[t - 1]) <= 1e-6 * max(1.0, orc.grad_norms[t - 1]), t
+    wk.flush()
+    assert abs(wk.grad_norm(13) - orc.grad_norms[13]) <= 1e-6 * max(1.0, orc.grad_norms[13])
+
+
 def test_engine_flush_midway_and_continue(pkg):
     _, E, L, Wk = pkg
     sizes = [2000, 17]
