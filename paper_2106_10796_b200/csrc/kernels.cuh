@@ -66,6 +66,42 @@ __device__ __forceinline__ uint32_t ld_word(const uint32_t* p) {
     return v;
 }
 
+// Masked 4-element accesses for the last (partial) chunk of a key: nv = valid elements
+// (>= 4: one vector access; 1..3: scalar accesses; missing loads read as 0). Lets the
+// vector paths take partial tiles too — a latency-bound per-element fallback on the
+// final tile of a launch (ResNet-50's fc bias) measured as a ~14 us straggler.
+__device__ __forceinline__ float4 ld_stream_m(const float* p, int nv) {
+    if (nv >= 4) return ld_stream(p);
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (nv > 0) v.x = p[0];
+    if (nv > 1) v.y = p[1];
+    if (nv > 2) v.z = p[2];
+    return v;
+}
+__device__ __forceinline__ d4 ld_stream_m(const double* p, int nv) {
+    if (nv >= 4) return ld_stream(p);
+    d4 v{0.0, 0.0, 0.0, 0.0};
+    if (nv > 0) v.x = p[0];
+    if (nv > 1) v.y = p[1];
+    if (nv > 2) v.z = p[2];
+    return v;
+}
+template <typename T>
+__device__ __forceinline__ void st_stream_m(T* p, T a, T b, T c, T d, int nv) {
+    if (nv >= 4) {
+        st_stream(p, a, b, c, d);
+        return;
+    }
+    if (nv > 0) p[0] = a;
+    if (nv > 1) p[1] = b;
+    if (nv > 2) p[2] = c;
+}
+// valid elements of the 4 starting at tile offset off, in a tile of ne elements
+__device__ __forceinline__ int nvalid4(int ne, int off) {
+    const int v = ne - off;
+    return v < 0 ? 0 : (v > 4 ? 4 : v);
+}
+
 __device__ __forceinline__ bool aligned_to(const void* p, uintptr_t a) {
     return (reinterpret_cast<uintptr_t>(p) & (a - 1)) == 0;
 }
@@ -411,8 +447,65 @@ __device__ __forceinline__ double apply_mean_general(const uint32_t* codes, int 
     return inv_n != 0.0 ? __dmul_rn(tot, inv_n) : __ddiv_rn(tot, static_cast<double>(nr));
 }
 
+// K2 vector path for one tile (exact-alpha table, compile-time rank count). Tiles of ne <
+// TILE_ELEMS elements (a key's last) use masked accesses; padding codes are ignored.
+template <int NR>
+__device__ __forceinline__ void apply_vec_tile(const ApplyQArgs& a, const float* s_upd, int nr, int lane,
+                                               int64_t e0, int64_t w0, int ne, int nw, bool do_loc, int so0,
+                                               int64_t sbnd, int& isq, double& gsq2, uint64_t& bad_idx) {
+    constexpr int R = NR > 0 ? NR : 1;
+    uint32_t wv[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) wv[r] = lane < nw ? ld_word(a.gathered + r * a.stride + w0 + lane) : 0u;
+    float4 wt[CHUNKS], gt[CHUNKS];
+#pragma unroll
+    for (int c = 0; c < CHUNKS; ++c) {
+        const int64_t e = e0 + 128 * c + 4 * lane;
+        const int nv = nvalid4(ne, 128 * c + 4 * lane);
+        wt[c] = ld_stream_m(a.W + e, nv);
+        if (do_loc) gt[c] = ld_stream_m(a.gnext + e, nv);
+    }
+#pragma unroll
+    for (int c = 0; c < CHUNKS; ++c) {
+        const int64_t e = e0 + 128 * c + 4 * lane;
+        const int nv = nvalid4(ne, 128 * c + 4 * lane);
+        Counts cnt{0u, 0u, 0u, 0u, 0u};
+#pragma unroll
+        for (int r = 0; r < R; ++r) count_add(cnt, __shfl_sync(FULL, wv[r], 8 * c + (lane >> 2)));
+        const int jb = 4 * (lane & 3);  // first code position of this lane in the word
+        float w4[4] = {wt[c].x, wt[c].y, wt[c].z, wt[c].w};
+        float g4[4];
+        if (do_loc) { g4[0] = gt[c].x; g4[1] = gt[c].y; g4[2] = gt[c].z; g4[3] = gt[c].w; }
+        float l4[4];
+        int cq[4];
+        lane_counts(cnt, lane, cq);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            w4[q] = __fsub_rn(w4[q], s_upd[cq[q] + nr]);
+            if (do_loc) l4[q] = __fmaf_rn(-a.eta_l, g4[q], w4[q]);
+            isq += cq[q] * cq[q];
+            if (a.fold_scale != 0.f) {  // N=1 correction round t+1: W_{t+2} = W_{t+1} - eta*g_{t+1}
+                w4[q] = __fmaf_rn(-a.fold_scale, g4[q], w4[q]);
+                const double m = static_cast<double>(g4[q]);
+                gsq2 = __fma_rn(m, m, gsq2);
+            }
+        }
+        const uint32_t vm = nv >= 4 ? 0xffu : (1u << (2 * nv)) - 1u;  // padding codes are not checked
+        if (((cnt.rsv >> (2 * jb)) & vm) != 0u) {
+            const int q = __ffs((cnt.rsv >> (2 * jb)) & vm & 0x55u) / 2;
+            const uint64_t idx = static_cast<uint64_t>(e + q);
+            bad_idx = idx < bad_idx ? idx : bad_idx;
+        }
+        if (nv > 0) {
+            st_stream_m(a.W + e, w4[0], w4[1], w4[2], w4[3], nv);
+            if (do_loc) st_stream_m(a.loc + e, l4[0], l4[1], l4[2], l4[3], nv);
+            if (a.gs.chunk != 0) st_stream_m(stage_at(a.gs, e, so0, sbnd), g4[0], g4[1], g4[2], g4[3], nv);
+        }
+    }
+}
+
 template <int NR>  // NR > 0: compile-time rank count; NR == 0: runtime (generic)
-__global__ void __launch_bounds__(256) k_apply_quant(ApplyQArgs a, KeyTab kt, DecodeTab tab) {
+__global__ void __launch_bounds__(256, 2) k_apply_quant(ApplyQArgs a, KeyTab kt, DecodeTab tab) {
     pdl_enter(a.gclear[0], a.gclear[1]);
     p2p_wait2(a.x, a.xs);
     const bool skip = a.err != nullptr && *reinterpret_cast<volatile uint64_t*>(a.err) < a.skip_below;
@@ -462,7 +555,7 @@ __global__ void __launch_bounds__(256) k_apply_quant(ApplyQArgs a, KeyTab kt, De
             const int ne = ne64 < TILE_ELEMS ? static_cast<int>(ne64) : TILE_ELEMS;
             const int64_t nw64 = kc.w1 - w0;
             const int nw = nw64 < TILE_WORDS ? static_cast<int>(nw64) : TILE_WORDS;
-            const bool fast = NR > 0 && a.exact && ne == TILE_ELEMS && aligned_to(a.W + e0, 16) &&
+            const bool fast = NR > 0 && a.exact && aligned_to(a.W + e0, 16) &&
                               (!do_loc || (aligned_to(a.gnext + e0, 16) && aligned_to(a.loc + e0, 16)));
             int so0 = 0;
             int64_t sbnd = 0;
@@ -471,50 +564,7 @@ __global__ void __launch_bounds__(256) k_apply_quant(ApplyQArgs a, KeyTab kt, De
                 sbnd = (so0 + 1) * a.gs.chunk;
             }
             if (fast) {
-                constexpr int R = NR > 0 ? NR : 1;
-                uint32_t wv[R];
-#pragma unroll
-                for (int r = 0; r < R; ++r) wv[r] = ld_word(a.gathered + r * a.stride + w0 + lane);
-                float4 wt[CHUNKS], gt[CHUNKS];
-#pragma unroll
-                for (int c = 0; c < CHUNKS; ++c) {
-                    const int64_t e = e0 + 128 * c + 4 * lane;
-                    wt[c] = ld_stream(a.W + e);
-                    if (do_loc) gt[c] = ld_stream(a.gnext + e);
-                }
-#pragma unroll
-                for (int c = 0; c < CHUNKS; ++c) {
-                    const int64_t e = e0 + 128 * c + 4 * lane;
-                    Counts cnt{0u, 0u, 0u, 0u, 0u};
-#pragma unroll
-                    for (int r = 0; r < R; ++r) count_add(cnt, __shfl_sync(FULL, wv[r], 8 * c + (lane >> 2)));
-                    const int jb = 4 * (lane & 3);  // first code position of this lane in the word
-                    float w4[4] = {wt[c].x, wt[c].y, wt[c].z, wt[c].w};
-                    float g4[4];
-                    if (do_loc) { g4[0] = gt[c].x; g4[1] = gt[c].y; g4[2] = gt[c].z; g4[3] = gt[c].w; }
-                    float l4[4];
-                    int cq[4];
-                    lane_counts(cnt, lane, cq);
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        w4[q] = __fsub_rn(w4[q], s_upd[cq[q] + nr]);
-                        if (do_loc) l4[q] = __fmaf_rn(-a.eta_l, g4[q], w4[q]);
-                        isq += cq[q] * cq[q];
-                        if (a.fold_scale != 0.f) {  // N=1 correction round t+1: W_{t+2} = W_{t+1} - eta*g_{t+1}
-                            w4[q] = __fmaf_rn(-a.fold_scale, g4[q], w4[q]);
-                            const double m = static_cast<double>(g4[q]);
-                            gsq2 = __fma_rn(m, m, gsq2);
-                        }
-                    }
-                    if (((cnt.rsv >> (2 * jb)) & 0xffu) != 0u) {
-                        const int q = __ffs((cnt.rsv >> (2 * jb)) & 0x55u) / 2;
-                        const uint64_t idx = static_cast<uint64_t>(e + q);
-                        bad_idx = idx < bad_idx ? idx : bad_idx;
-                    }
-                    st_stream(a.W + e, w4[0], w4[1], w4[2], w4[3]);
-                    if (do_loc) st_stream(a.loc + e, l4[0], l4[1], l4[2], l4[3]);
-                    if (a.gs.chunk != 0) st_stream(stage_at(a.gs, e, so0, sbnd), g4[0], g4[1], g4[2], g4[3]);
-                }
+                apply_vec_tile<NR>(a, s_upd, nr, lane, e0, w0, ne, nw, do_loc, so0, sbnd, isq, gsq2, bad_idx);
             } else {
                 // generic path: lane l owns element 32s + l; word (2s + l/16), code l%16
                 uint32_t wv[MAX_RANKS];

@@ -46,6 +46,117 @@ struct FusedArgs {
     double* gclear[2];    // grad-norm ring slots to zero (see pdl_enter), nullable
 };
 
+// One task of the vector path: CH chunks of 128 elements (from chunk c0) of the tile at
+// element e0 / word w0, all loads issued before any use. A key's last tile (ne < TILE_ELEMS
+// elements) uses masked accesses; padding quantizes to code 00 (the
+// reference's zero padding of the last word, codec.py:131-143) and is never stored.
+template <int NR, int APPLY, int CH>
+__device__ __forceinline__ uint32_t fused_vec_task(const FusedArgs& a, const float* s_upd, int lane, int64_t e0,
+                                                   int64_t w0, int ne, int nw, int c0, bool a_off, bool q_off,
+                                                   uint32_t ahi, uint32_t alo, uint64_t& bad_idx, uint64_t& bad_sym,
+                                                   double& gsq, int& isq) {
+    uint32_t myword = 0;
+    float4 gv[CH], wv[CH], sv[CH];
+    d4 rv[CH];
+    uint32_t cw[APPLY == APPLY_Q ? NR : 1];
+    if constexpr (APPLY == APPLY_Q) {
+#pragma unroll
+        for (int r = 0; r < NR; ++r)
+            cw[r] = lane < nw ? ld_word(a.gathered + r * a.stride + w0 + lane) : 0u;
+    }
+#pragma unroll
+    for (int c = 0; c < CH; ++c) {
+        const int64_t e = e0 + 128 * (c0 + c) + 4 * lane;
+        const int nv = nvalid4(ne, 128 * (c0 + c) + 4 * lane);
+        gv[c] = ld_stream_m(a.g + e, nv);
+        rv[c] = ld_stream_m(a.r_in + e, nv);
+        wv[c] = ld_stream_m(a.W + e, nv);
+        if constexpr (APPLY == APPLY_F) sv[c] = ld_stream_m(a.gsum + e, nv);
+    }
+    uint32_t v[CH];
+    bool bad = false;
+#pragma unroll
+    for (int c = 0; c < CH; ++c) {
+        const int64_t e = e0 + 128 * (c0 + c) + 4 * lane;
+        const int nv = nvalid4(ne, 128 * (c0 + c) + 4 * lane);
+        float g4[4] = {gv[c].x, gv[c].y, gv[c].z, gv[c].w};
+        float w4[4] = {wv[c].x, wv[c].y, wv[c].z, wv[c].w};
+        double r4[4] = {rv[c].x, rv[c].y, rv[c].z, rv[c].w};
+        if (!a_off) {
+            float l4[4];
+            if constexpr (APPLY == APPLY_Q) {
+                Counts cnt{0u, 0u, 0u, 0u, 0u};
+#pragma unroll
+                for (int r = 0; r < NR; ++r) count_add(cnt, __shfl_sync(FULL, cw[r], 8 * (c0 + c) + (lane >> 2)));
+                int cq[4];
+                lane_counts(cnt, lane, cq);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    w4[q] = __fsub_rn(w4[q], s_upd[cq[q] + NR]);
+                    l4[q] = __fmaf_rn(-a.eta_l, g4[q], w4[q]);
+                    isq += cq[q] * cq[q];
+                }
+                const int jb = 4 * (lane & 3);
+                const uint32_t vm = nv >= 4 ? 0xffu : (1u << (2 * nv)) - 1u;  // padding codes are not checked
+                if (((cnt.rsv >> (2 * jb)) & vm) != 0u) {
+                    const int q = __ffs((cnt.rsv >> (2 * jb)) & vm & 0x55u) / 2;
+                    bad_sym = static_cast<uint64_t>(e + q) < bad_sym ? static_cast<uint64_t>(e + q) : bad_sym;
+                }
+            } else if constexpr (APPLY == APPLY_F) {
+                const float s4[4] = {sv[c].x, sv[c].y, sv[c].z, sv[c].w};
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    w4[q] = __fmaf_rn(-a.scale, s4[q], w4[q]);
+                    l4[q] = __fmaf_rn(-a.eta_l, g4[q], w4[q]);
+                    if (a.gnorm != nullptr) {
+                        const double m = s4[q] * a.inv_n;
+                        gsq = __fma_rn(m, m, gsq);
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int q = 0; q < 4; ++q) l4[q] = __fmaf_rn(-a.eta_l, g4[q], w4[q]);
+            }
+            if constexpr (APPLY != APPLY_L) st_stream_m(a.W + e, w4[0], w4[1], w4[2], w4[3], nv);
+            st_stream_m(a.loc + e, l4[0], l4[1], l4[2], l4[3], nv);
+        }
+        if (!q_off) {
+            double o[4];
+            uint32_t code = 0;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) code |= quant1_lean(r4[q], g4[q], a.alpha, ahi, alo, o[q], bad) << (2 * q);
+            st_stream_m(a.r_out + e, o[0], o[1], o[2], o[3], nv);
+            v[c] = code << (8 * (lane & 3));
+        } else {
+            v[c] = 0;
+        }
+    }
+    if (__any_sync(FULL, bad)) {
+#pragma unroll
+        for (int c = 0; c < CH; ++c) {
+            const float g4[4] = {gv[c].x, gv[c].y, gv[c].z, gv[c].w};
+            const double r4[4] = {rv[c].x, rv[c].y, rv[c].z, rv[c].w};
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                if (nonfinite(__dadd_rn(r4[q], static_cast<double>(g4[q])))) {
+                    const uint64_t idx =
+                        a.tag | static_cast<uint64_t>(e0 + 128 * (c0 + c) + 4 * lane + q);
+                    bad_idx = idx < bad_idx ? idx : bad_idx;
+                }
+        }
+    }
+#pragma unroll
+    for (int c = 0; c < CH; ++c) v[c] |= __shfl_xor_sync(FULL, v[c], 1);
+#pragma unroll
+    for (int c = 0; c < CH; ++c) v[c] |= __shfl_xor_sync(FULL, v[c], 2);
+#pragma unroll
+    for (int c = 0; c < CH; ++c) {
+        const uint32_t w = __shfl_sync(FULL, v[c], 4 * (lane & 7));
+        if ((lane >> 3) == c0 + c) myword = w;
+    }
+    return myword;
+}
+
 // Data moved with 128/256-bit coalesced loads straight into registers (all loads of a
 // tile issued first), two 256-thread CTAs per SM, dynamic tile scheduling.
 // CH = chunks of 128 elements per task: 4 (a whole tile) for large layouts, 1 for small
@@ -109,106 +220,14 @@ __global__ void __launch_bounds__(256, 2) k_fused_ldg(FusedArgs a, KeyTab kt, De
             const int ne = ne64 < TILE_ELEMS ? static_cast<int>(ne64) : TILE_ELEMS;
             const int64_t nw64 = cc.w1 - w0;
             const int nw = nw64 < TILE_WORDS ? static_cast<int>(nw64) : TILE_WORDS;
-            const bool fast = ne == TILE_ELEMS && aligned_to(a.g + e0, 16) && aligned_to(a.r_in + e0, 32) &&
+            const bool fast = aligned_to(a.g + e0, 16) && aligned_to(a.r_in + e0, 32) &&
                               aligned_to(a.r_out + e0, 32) && aligned_to(a.W + e0, 16) && aligned_to(a.loc + e0, 16) &&
                               (APPLY != APPLY_F || aligned_to(a.gsum + e0, 16));
-            if (!fast && c0 != 0) continue;  // partial / misaligned tiles: one task does the whole tile
+            if (!fast && c0 != 0) continue;  // misaligned tiles: one task does the whole tile
             uint32_t myword = 0;
             if (fast) {
-                float4 gv[CH], wv[CH], sv[CH];
-                d4 rv[CH];
-                uint32_t cw[APPLY == APPLY_Q ? NR : 1];
-                if constexpr (APPLY == APPLY_Q) {
-#pragma unroll
-                    for (int r = 0; r < NR; ++r) cw[r] = ld_word(a.gathered + r * a.stride + w0 + lane);
-                }
-#pragma unroll
-                for (int c = 0; c < CH; ++c) {
-                    const int64_t e = e0 + 128 * (c0 + c) + 4 * lane;
-                    gv[c] = ld_stream(a.g + e);
-                    rv[c] = ld_stream(a.r_in + e);
-                    wv[c] = ld_stream(a.W + e);
-                    if constexpr (APPLY == APPLY_F) sv[c] = ld_stream(a.gsum + e);
-                }
-                uint32_t v[CH];
-                bool bad = false;
-#pragma unroll
-                for (int c = 0; c < CH; ++c) {
-                    const int64_t e = e0 + 128 * (c0 + c) + 4 * lane;
-                    float g4[4] = {gv[c].x, gv[c].y, gv[c].z, gv[c].w};
-                    float w4[4] = {wv[c].x, wv[c].y, wv[c].z, wv[c].w};
-                    double r4[4] = {rv[c].x, rv[c].y, rv[c].z, rv[c].w};
-                    if (!a_off) {
-                        float l4[4];
-                        if constexpr (APPLY == APPLY_Q) {
-                            Counts cnt{0u, 0u, 0u, 0u, 0u};
-#pragma unroll
-                            for (int r = 0; r < NR; ++r) count_add(cnt, __shfl_sync(FULL, cw[r], 8 * (c0 + c) + (lane >> 2)));
-                            int cq[4];
-                            lane_counts(cnt, lane, cq);
-#pragma unroll
-                            for (int q = 0; q < 4; ++q) {
-                                w4[q] = __fsub_rn(w4[q], s_upd[cq[q] + NR]);
-                                l4[q] = __fmaf_rn(-a.eta_l, g4[q], w4[q]);
-                                isq += cq[q] * cq[q];
-                            }
-                            const int jb = 4 * (lane & 3);
-                            if (((cnt.rsv >> (2 * jb)) & 0xffu) != 0u) {
-                                const int q = __ffs((cnt.rsv >> (2 * jb)) & 0x55u) / 2;
-                                bad_sym = static_cast<uint64_t>(e + q) < bad_sym ? static_cast<uint64_t>(e + q) : bad_sym;
-                            }
-                        } else if constexpr (APPLY == APPLY_F) {
-                            const float s4[4] = {sv[c].x, sv[c].y, sv[c].z, sv[c].w};
-#pragma unroll
-                            for (int q = 0; q < 4; ++q) {
-                                w4[q] = __fmaf_rn(-a.scale, s4[q], w4[q]);
-                                l4[q] = __fmaf_rn(-a.eta_l, g4[q], w4[q]);
-                                if (a.gnorm != nullptr) {
-                                    const double m = s4[q] * a.inv_n;
-                                    gsq = __fma_rn(m, m, gsq);
-                                }
-                            }
-                        } else {
-#pragma unroll
-                            for (int q = 0; q < 4; ++q) l4[q] = __fmaf_rn(-a.eta_l, g4[q], w4[q]);
-                        }
-                        if constexpr (APPLY != APPLY_L) st_stream(a.W + e, w4[0], w4[1], w4[2], w4[3]);
-                        st_stream(a.loc + e, l4[0], l4[1], l4[2], l4[3]);
-                    }
-                    if (!q_off) {
-                        double o[4];
-                        uint32_t code = 0;
-#pragma unroll
-                        for (int q = 0; q < 4; ++q) code |= quant1_lean(r4[q], g4[q], a.alpha, ahi, alo, o[q], bad) << (2 * q);
-                        st_stream(a.r_out + e, o[0], o[1], o[2], o[3]);
-                        v[c] = code << (8 * (lane & 3));
-                    } else {
-                        v[c] = 0;
-                    }
-                }
-                if (__any_sync(FULL, bad)) {
-#pragma unroll
-                    for (int c = 0; c < CH; ++c) {
-                        const float g4[4] = {gv[c].x, gv[c].y, gv[c].z, gv[c].w};
-                        const double r4[4] = {rv[c].x, rv[c].y, rv[c].z, rv[c].w};
-#pragma unroll
-                        for (int q = 0; q < 4; ++q)
-                            if (nonfinite(__dadd_rn(r4[q], static_cast<double>(g4[q])))) {
-                                const uint64_t idx =
-                                    a.tag | static_cast<uint64_t>(e0 + 128 * (c0 + c) + 4 * lane + q);
-                                bad_idx = idx < bad_idx ? idx : bad_idx;
-                            }
-                    }
-                }
-#pragma unroll
-                for (int c = 0; c < CH; ++c) v[c] |= __shfl_xor_sync(FULL, v[c], 1);
-#pragma unroll
-                for (int c = 0; c < CH; ++c) v[c] |= __shfl_xor_sync(FULL, v[c], 2);
-#pragma unroll
-                for (int c = 0; c < CH; ++c) {
-                    const uint32_t w = __shfl_sync(FULL, v[c], 4 * (lane & 7));
-                    if ((lane >> 3) == c0 + c) myword = w;
-                }
+                myword = fused_vec_task<NR, APPLY, CH>(a, s_upd, lane, e0, w0, ne, nw, c0, a_off, q_off, ahi, alo,
+                                                       bad_idx, bad_sym, gsq, isq);
             } else {
                 uint32_t cw[APPLY == APPLY_Q ? NR : 1];
                 if constexpr (APPLY == APPLY_Q) {
