@@ -11,7 +11,8 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libcdsgd_b200.so")
+# CDSGD_LIB: load another build of the same library (development A/B of kernel variants)
+LIB_PATH = os.environ.get("CDSGD_LIB") or os.path.join(_HERE, "libcdsgd_b200.so")
 
 OK = 0
 ERR_ARG, ERR_CUDA, ERR_NCCL, ERR_STATE, ERR_NUMERIC, ERR_CORRUPT = -1, -2, -3, -4, -5, -6

@@ -50,8 +50,8 @@ def up_to_date() -> bool:
     return all(os.path.getmtime(d) <= t for d in deps())
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and up_to_date():
+def build(force: bool = False, verbose: bool = False, out: str = LIB) -> str:
+    if out == LIB and not force and up_to_date():
         return LIB
     nd = nccl_dir()
     nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
@@ -59,7 +59,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         nvcc, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC",
         "-Xptxas", "-v" if verbose else "-O3",
         "-I", INCLUDE, "-I", CSRC, "-I", os.path.join(nd, "include"),
-        *sources(), "-o", LIB + ".tmp",
+        *sources(), "-o", out + ".tmp",
         "-L", os.path.join(nd, "lib"), "-l:libnccl.so.2", "-Xlinker", "-rpath=" + os.path.join(nd, "lib"),
     ]
     res = subprocess.run(cmd, capture_output=True, text=True)
@@ -67,9 +67,10 @@ def build(force: bool = False, verbose: bool = False) -> str:
         raise RuntimeError("nvcc failed:\n" + " ".join(cmd) + "\n" + res.stdout + res.stderr)
     if verbose:
         print(res.stdout + res.stderr)
-    os.replace(LIB + ".tmp", LIB)
-    return LIB
+    os.replace(out + ".tmp", out)
+    return out
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    outs = [a.split("=", 1)[1] for a in sys.argv[1:] if a.startswith("--out=")]
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, out=outs[0] if outs else LIB))

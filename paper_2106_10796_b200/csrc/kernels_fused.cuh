@@ -184,7 +184,9 @@ __global__ void __launch_bounds__(256, 2) k_fused_ldg(FusedArgs a, KeyTab kt, De
     // Dynamic schedule: warps claim CLAIM consecutive tasks at a time from a global ticket,
     // so the kernel ends when the work does, not when the slowest static range does.
     // small layouts (fewer than ~4 tasks per warp): claim single tasks for parallelism
-    const unsigned CLAIM = ntasks < 4 * ((int64_t)gridDim.x * blockDim.x / 32) ? 1u : 2u;
+    const int64_t nwarps = (int64_t)gridDim.x * blockDim.x / 32;
+    const unsigned CLAIM = ntasks < 4 * nwarps ? 1u : 2u;
+    const int64_t tail_from = ntasks - nwarps;
     const bool dyn = a.sched != nullptr;
     int64_t cbase = 0, cend = 0;
     if (dyn) {
@@ -200,13 +202,14 @@ __global__ void __launch_bounds__(256, 2) k_fused_ldg(FusedArgs a, KeyTab kt, De
         cc.seek(kt, tb / SPL);
         for (int64_t task = tb; task < te; ++task) {
             if (dyn) {
-                if (task >= cend) {  // claim the next batch
+                if (task >= cend) {  // claim the next batch (single tasks in the last ~one per warp)
+                    const unsigned cl = task < tail_from ? CLAIM : 1u;
                     unsigned t0 = 0;
-                    if (lane == 0) t0 = atomicAdd(a.sched, CLAIM);
+                    if (lane == 0) t0 = atomicAdd(a.sched, cl);
                     const int64_t nb = __shfl_sync(FULL, t0, 0);
                     if (nb >= ntasks) break;
                     task = nb;
-                    cend = nb + (int64_t)CLAIM < ntasks ? nb + (int64_t)CLAIM : ntasks;
+                    cend = nb + (int64_t)cl < ntasks ? nb + (int64_t)cl : ntasks;
                 }
             }
             const int64_t ti = task / SPL;
