@@ -1232,6 +1232,7 @@ extern "C" int cdsgd_engine_step(cdsgd_engine* E, const float* g, void* stream) 
             a.xa.sc_fence = E->sc_fence;
             a.xa.err = E->d.err;
             if (E->diag_no_wait) a.xq.wait_value = a.xa.wait_value = 0;
+            if (!has_pend) a.xa.nranks = 0;  // nothing to consume (local-only pass)
             E->last_use[p] = t;
         }
         E->rlog.push_back(static_cast<int8_t>(E->rcur));
