@@ -59,6 +59,7 @@ def build(force: bool = False, verbose: bool = False, out: str = LIB) -> str:
         nvcc, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC",
         "-Xptxas", "-v" if verbose else "-O3",
         "-I", INCLUDE, "-I", CSRC, "-I", os.path.join(nd, "include"),
+        *os.environ.get("CDSGD_NVCC_FLAGS", "").split(),  # development A/B builds (-D...)
         *sources(), "-o", out + ".tmp",
         "-L", os.path.join(nd, "lib"), "-l:libnccl.so.2", "-Xlinker", "-rpath=" + os.path.join(nd, "lib"),
     ]
