@@ -505,7 +505,12 @@ __device__ __forceinline__ void apply_vec_tile(const ApplyQArgs& a, const float*
 }
 
 template <int NR>  // NR > 0: compile-time rank count; NR == 0: runtime (generic)
-__global__ void __launch_bounds__(256, 2) k_apply_quant(ApplyQArgs a, KeyTab kt, DecodeTab tab) {
+// 3 CTAs per SM at N=1 (80 registers, a 24-byte spill): 88 -> 82 us at ResNet-50 size, the
+// extra warps keep more loads in flight; more ranks spill more, so they keep 2.
+#ifndef CDSGD_K2_MINB
+#define CDSGD_K2_MINB (NR == 1 ? 3 : 2)
+#endif
+__global__ void __launch_bounds__(256, CDSGD_K2_MINB) k_apply_quant(ApplyQArgs a, KeyTab kt, DecodeTab tab) {
     pdl_enter(a.gclear[0], a.gclear[1]);
     p2p_wait2(a.x, a.xs);
     const bool skip = a.err != nullptr && *reinterpret_cast<volatile uint64_t*>(a.err) < a.skip_below;
