@@ -32,8 +32,12 @@ class CDSGDModule:
         if any(p.dtype != torch.float32 for p in self.params):
             raise TypeError("CD-SGD weights are fp32 (the codec itself runs in fp64)")
         self.layout = from_module(module)
+        self._view_cache = {}
         dev = torch.device(device) if device is not None else self.params[0].device
-        w0 = torch.cat([p.detach().reshape(-1) for p in self.params]).to(dev)
+        w0 = torch.empty(self.layout.total, dtype=torch.float32, device=dev)
+        with torch.no_grad():
+            for v, p in zip(self._make_views(w0), self.params):
+                v.copy_(p.detach())
         self.worker = CDSGDWorker(self.layout, hp, w0, rank=rank, comm=comm, exchange=exchange, device=dev,
                                   **worker_kw)
         # round t's gradient stays readable until round t+1 is applied: two buffers alternate
@@ -42,7 +46,26 @@ class CDSGDModule:
         self._load(self.worker.compute_weights())
 
     def _views(self, flat: torch.Tensor):
-        return [flat[s.start:s.start + s.length].view_as(p) for s, p in zip(self.layout.spans, self.params)]
+        """Cached per buffer: the SAME view objects are bound as .grad, so step() can tell
+        by identity that autograd accumulated in place (no copy)."""
+        key = (flat.data_ptr(), flat.numel())
+        v = self._view_cache.get(key)
+        if v is None:
+            v = self._view_cache[key] = self._make_views(flat)
+        return v
+
+    def _make_views(self, flat: torch.Tensor):
+        """Each parameter's key as a view of a flat buffer with the PARAMETER's strides, so a
+        channels_last weight keeps its memory order in W / loc / the gradient (the codec is
+        elementwise per key: element order inside a key is the caller's choice). Parameter
+        loads and autograd's gradient accumulation then need no layout conversion."""
+        out = []
+        for s, p in zip(self.layout.spans, self.params):
+            if p.is_contiguous() or not (p.dim() == 4 and p.is_contiguous(memory_format=torch.channels_last)):
+                out.append(flat[s.start:s.start + s.length].view_as(p))
+            else:
+                out.append(flat.as_strided(p.shape, p.stride(), flat.storage_offset() + s.start))
+        return out
 
     def _bind_grads(self, i: int) -> None:
         buf = self._grads[i]
@@ -51,9 +74,9 @@ class CDSGDModule:
             p.grad = v
 
     def _load(self, flat: torch.Tensor) -> None:
+        # one multi-tensor launch instead of a copy per parameter (ResNet-50: 161 launches)
         with torch.no_grad():
-            for p, v in zip(self.params, self._views(flat)):
-                p.copy_(v)
+            torch._foreach_copy_(self.params, self._views(flat))
 
     @property
     def t(self) -> int:
@@ -65,7 +88,8 @@ class CDSGDModule:
         g = self._grads[t % 2]
         for p, v in zip(self.params, self._views(g)):
             if p.grad is not v and p.grad is not None:
-                v.copy_(p.grad)  # an optimizer or user replaced .grad: fall back to a copy
+                with torch.no_grad():
+                    v.copy_(p.grad)  # an optimizer or user replaced .grad: fall back to a copy
         self.worker.step(g)
         self._bind_grads((t + 1) % 2)
         self._load(self.worker.compute_weights())

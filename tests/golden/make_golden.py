@@ -9,6 +9,8 @@ It imports ``cdsgd`` from ``/root/reference/pkg/src`` and writes
 * ``codec_golden.npz``  — ``codec.quantize`` / ``dequantize`` / ``pack_symbols`` cases
   (codec.py:140-206), including ties, signed zeros, |a| >= 2*alpha, subnormals,
   non-finite error indices and reserved-symbol error indices;
+* ``costmodel_golden.npz`` — the time model (costmodel.py:51-152) over a grid of
+  timing constants (``--only-costmodel`` regenerates just this file);
 * ``engine_golden.npz`` — lock-step engine traces (engine.py:614-663) on synthetic
   gradients: ``loss_and_grad`` (engine.py:363) is the ONLY thing replaced, by a
   function that returns the pre-drawn gradient for call (t, w); Worker,
@@ -228,7 +230,41 @@ def wire_cases():
     return out
 
 
+def costmodel_cases():
+    """Eq. 6-9 over a grid of timing constants that hits every case and the ties
+    (costmodel.py:51-152): averages, per-iteration comm / time / savings, regime, and
+    the cumulative timeline."""
+    import itertools
+    import warnings
+
+    import cdsgd.costmodel as cm
+
+    vals = (0.0, 0.5, 1.0, 1.5, 3.0)
+    params, avg, per_i, regime, cum = [], [], [], [], []
+    for tau, phi, psi, delta in itertools.product(vals, vals, vals, (0.0, 0.25, 1.0)):
+        for k in (1, 2, 4, 5):
+            with warnings.catch_warnings():
+                warnings.simplefilter("ignore")
+                p = cm.CostParams(tau=tau, phi=phi, psi=psi, delta=delta, k=k)
+            params.append((tau, phi, psi, delta, k))
+            avg.append((cm.t_ssgd(p), cm.t_loc(p), cm.t_bit(p), cm.avg_cd(p)))
+            rows = []
+            for i in range(1, 11):
+                rows.append((cm.comm_cd(i, p), cm.t_cd(i, p), cm.saving_vs_loc(i, p), cm.saving_vs_bit(i, p)))
+            per_i.append(rows)
+            regime.append(cm.classify_regime(p))
+            tl = cm.timeline(p, 10)
+            cum.append([r[3] for r in tl])
+    return {"cm_params": np.array(params, dtype=np.float64), "cm_avg": np.array(avg),
+            "cm_per_i": np.array(per_i), "cm_regime": np.array(regime), "cm_timeline_cum": np.array(cum)}
+
+
 def main():
+    if "--only-costmodel" in sys.argv:
+        np.savez_compressed(os.path.join(HERE, "costmodel_golden.npz"), **costmodel_cases())
+        print("wrote costmodel_golden.npz")
+        return
+    np.savez_compressed(os.path.join(HERE, "costmodel_golden.npz"), **costmodel_cases())
     codec_out = codec_cases()
     codec_out.update(wire_cases())
     np.savez_compressed(os.path.join(HERE, "codec_golden.npz"), **codec_out)
