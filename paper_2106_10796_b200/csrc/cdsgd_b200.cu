@@ -68,12 +68,24 @@ DeviceInfo& dev_info() {
     }
     return di;
 }
+// Resident CTAs of a kernel, cached per (kernel, block size, device): the occupancy query
+// is a driver call, and launch-bound layouts (ResNet-20) pay for every host microsecond.
 template <typename K>
 int resident_blocks(K kernel, int threads) {
+    struct Entry { const void* k; int threads, dev, blocks; };
+    static thread_local Entry cache[64];
+    static thread_local int used = 0;
+    int d = 0;
+    cudaGetDevice(&d);
+    for (int i = 0; i < used; ++i)
+        if (cache[i].k == reinterpret_cast<const void*>(kernel) && cache[i].threads == threads && cache[i].dev == d)
+            return cache[i].blocks;
     int per_sm = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, 0) != cudaSuccess || per_sm < 1)
         per_sm = 1;
-    return per_sm * dev_info().sms;
+    const int blocks = per_sm * dev_info().sms;
+    if (used < 64) cache[used++] = Entry{reinterpret_cast<const void*>(kernel), threads, d, blocks};
+    return blocks;
 }
 constexpr int THREADS = 256;
 constexpr int WARPS_PER_BLOCK = THREADS / 32;

@@ -34,6 +34,16 @@ from .codec import CodecNumericError, CorruptPayloadError, _locate
 from .engine import ConfigError, HyperParams, SchedulingError
 from .layout import Layout
 
+_RAW_STREAM = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+
+
+def _raw_stream(index: int) -> int:
+    """cudaStream_t of the current torch stream on device `index` (the per-step host path:
+    ~3 us cheaper than torch.cuda.current_stream(device).cuda_stream)."""
+    if _RAW_STREAM is not None:
+        return _RAW_STREAM(index)
+    return torch.cuda.current_stream(index).cuda_stream
+
 
 class CDSGDWorker:
     def __init__(
@@ -65,6 +75,7 @@ class CDSGDWorker:
             raise ConfigError("comm size/rank do not match hp.workers/rank")
         self.comm = comm
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self._dev_index = self.device.index if self.device.index is not None else torch.cuda.current_device()
         dev = self.device
         n, nw = layout.total, layout.n_words
         w0 = init_weights if isinstance(init_weights, torch.Tensor) else torch.from_numpy(np.asarray(init_weights))
@@ -114,7 +125,8 @@ class CDSGDWorker:
                 self._attach_p2p(group, exact=exchange == "p2p-exact")
             elif self.world > 1 and exchange != "nccl":
                 raise ConfigError(f"exchange must be 'p2p', 'p2p-exact' or 'nccl', got {exchange!r}")
-        self._keep: list[torch.Tensor] = []  # gradients still read by in-flight rounds
+        self._keep: list = [None, None]  # the last two gradients: still read by in-flight rounds
+        self._nstep = 0
         self.check_every = int(check_every)
         self._since_check = 0
         self._lib = _lib.lib()
@@ -208,7 +220,7 @@ class CDSGDWorker:
     def step(self, grad: torch.Tensor) -> None:
         if grad.dtype != torch.float32 or not grad.is_cuda or not grad.is_contiguous() or grad.numel() != self.layout.total:
             raise ConfigError("gradient must be a contiguous fp32 CUDA tensor of layout.total elements")
-        rc = self._lib.cdsgd_engine_step(self._eng, grad.data_ptr(), torch.cuda.current_stream(self.device).cuda_stream)
+        rc = self._lib.cdsgd_engine_step(self._eng, grad.data_ptr(), _raw_stream(self._dev_index))
         if rc != _lib.OK:
             msg = _lib.last_error()
             if rc == _lib.ERR_STATE:
@@ -216,9 +228,8 @@ class CDSGDWorker:
             if rc == _lib.ERR_ARG:
                 raise ConfigError(msg)
             raise _lib.LibraryError(msg, rc)
-        self._keep.append(grad)
-        if len(self._keep) > 2:
-            del self._keep[0]
+        self._keep[self._nstep & 1] = grad
+        self._nstep += 1
         if self.check_every:
             self._since_check += 1
             if self._since_check >= self.check_every:
