@@ -535,10 +535,9 @@ __global__ void __launch_bounds__(256, CDSGD_K2_MINB) k_apply_quant(ApplyQArgs a
     const int64_t tail_from = kt.ntiles - nwarps;  // single-tile claims from here on
     const bool dyn = a.sched != nullptr;
     int64_t cend = 0;
-    if (dyn) {  // warps claim CLAIM tiles at a time from a global ticket (see k_fused_ldg)
-        unsigned t0 = 0;
-        if (lane == 0) t0 = atomicAdd(a.sched, CLAIM);
-        tb = __shfl_sync(FULL, t0, 0);
+    const int64_t first_dyn = nwarps * CLAIM;  // first claim static, then tickets (see k_fused_ldg)
+    if (dyn) {
+        tb = ((static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5) * CLAIM;
         cend = tb + (int64_t)CLAIM < kt.ntiles ? tb + (int64_t)CLAIM : kt.ntiles;
         te = tb < kt.ntiles ? kt.ntiles : tb;
     }
@@ -550,7 +549,7 @@ __global__ void __launch_bounds__(256, CDSGD_K2_MINB) k_apply_quant(ApplyQArgs a
                 const unsigned cl = ti < tail_from ? CLAIM : 1u;
                 unsigned t0 = 0;
                 if (lane == 0) t0 = atomicAdd(a.sched, cl);
-                const int64_t nb = __shfl_sync(FULL, t0, 0);
+                const int64_t nb = first_dyn + static_cast<int64_t>(__shfl_sync(FULL, t0, 0));
                 if (nb >= kt.ntiles) break;
                 ti = nb;
                 cend = nb + (int64_t)cl < kt.ntiles ? nb + (int64_t)cl : kt.ntiles;

@@ -189,10 +189,12 @@ __global__ void __launch_bounds__(256, 2) k_fused_ldg(FusedArgs a, KeyTab kt, De
     const int64_t tail_from = ntasks - nwarps;
     const bool dyn = a.sched != nullptr;
     int64_t cbase = 0, cend = 0;
+    // first claim static (warp w: tasks [w*CLAIM, (w+1)*CLAIM)), later claims from the ticket
+    // offset by nwarps*CLAIM: no burst of one atomic per warp on a single counter at launch
+    // (it serialised ~2,400 warps for several us on ResNet-20-sized layouts)
+    const int64_t first_dyn = nwarps * CLAIM;
     if (dyn) {
-        unsigned t0 = 0;
-        if (lane == 0) t0 = atomicAdd(a.sched, CLAIM);
-        cbase = __shfl_sync(FULL, t0, 0);
+        cbase = ((static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5) * CLAIM;
         cend = cbase + (int64_t)CLAIM < ntasks ? cbase + (int64_t)CLAIM : ntasks;
         tb = cbase;
         te = cbase < ntasks ? ntasks : cbase;  // loop bound; real bound checked per claim
@@ -206,7 +208,7 @@ __global__ void __launch_bounds__(256, 2) k_fused_ldg(FusedArgs a, KeyTab kt, De
                     const unsigned cl = task < tail_from ? CLAIM : 1u;
                     unsigned t0 = 0;
                     if (lane == 0) t0 = atomicAdd(a.sched, cl);
-                    const int64_t nb = __shfl_sync(FULL, t0, 0);
+                    const int64_t nb = first_dyn + static_cast<int64_t>(__shfl_sync(FULL, t0, 0));
                     if (nb >= ntasks) break;
                     task = nb;
                     cend = nb + (int64_t)cl < ntasks ? nb + (int64_t)cl : ntasks;
