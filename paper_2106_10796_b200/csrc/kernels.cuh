@@ -146,6 +146,31 @@ struct TileCursor {
         }
         load(kt, lo);
     }
+    // Warp-collective seek (every lane calls it with the same tile): 32 candidate keys per
+    // round, so <= 1024 keys take two dependent loads instead of log2(nkeys). On small
+    // layouts this search was most of a warp's latency chain before its first tile.
+    __device__ __forceinline__ void seek_warp(const KeyTab& kt, int64_t tile, int lane) {
+        int lo = 0, hi = kt.nkeys - 1;  // toff[lo] <= tile; the answer is in [lo, hi]
+        while (lo < hi) {
+            const int step = (hi - lo + 32) / 32;
+            const int cand = lo + lane * step < hi ? lo + lane * step : hi;
+            const unsigned ok = __ballot_sync(0xffffffffu, __ldg(kt.toff + cand) <= tile);
+            const int last = 31 - __clz(ok);  // lane 0 (cand == lo) always qualifies
+            const int nlo = lo + last * step < hi ? lo + last * step : hi;
+            const int nhi = lo + (last + 1) * step - 1 < hi ? lo + (last + 1) * step - 1 : hi;
+            lo = nlo;
+            hi = last == 31 ? hi : nhi;
+        }
+        load(kt, lo);
+    }
+    // Warp-collective forward move: the next key directly, or a seek for a longer jump
+    // (dynamically scheduled warps jump ~2 tiles x #warps between claims: walking key by
+    // key cost one dependent load per key — ~800 per claim on a 2,000-key layout).
+    __device__ __forceinline__ void advance_warp(const KeyTab& kt, int64_t tile, int lane) {
+        if (tile < t1) return;
+        if (k + 2 > kt.nkeys || tile < __ldg(kt.toff + k + 2)) load(kt, k + 1);
+        else seek_warp(kt, tile, lane);
+    }
     __device__ __forceinline__ void advance_to(const KeyTab& kt, int64_t tile) {
         while (tile >= t1) load(kt, k + 1);
     }
@@ -543,7 +568,7 @@ __global__ void __launch_bounds__(256, CDSGD_K2_MINB) k_apply_quant(ApplyQArgs a
     }
     if (tb < te && !skip) {
         TileCursor kc;
-        kc.seek(kt, tb);
+        kc.seek_warp(kt, tb, lane);
         for (int64_t ti = tb; ti < te; ++ti) {
             if (dyn && ti >= cend) {
                 const unsigned cl = ti < tail_from ? CLAIM : 1u;
@@ -554,7 +579,7 @@ __global__ void __launch_bounds__(256, CDSGD_K2_MINB) k_apply_quant(ApplyQArgs a
                 ti = nb;
                 cend = nb + (int64_t)cl < kt.ntiles ? nb + (int64_t)cl : kt.ntiles;
             }
-            kc.advance_to(kt, ti);
+            kc.advance_warp(kt, ti, lane);
             const int64_t j = ti - kc.t0;
             const int64_t e0 = kc.e0 + j * TILE_ELEMS;
             const int64_t w0 = kc.w0 + j * TILE_WORDS;

@@ -201,7 +201,7 @@ __global__ void __launch_bounds__(256, 2) k_fused_ldg(FusedArgs a, KeyTab kt, De
     }
     if (tb < te) {
         TileCursor cc;
-        cc.seek(kt, tb / SPL);
+        cc.seek_warp(kt, tb / SPL, lane);
         for (int64_t task = tb; task < te; ++task) {
             if (dyn) {
                 if (task >= cend) {  // claim the next batch (single tasks in the last ~one per warp)
@@ -216,8 +216,8 @@ __global__ void __launch_bounds__(256, 2) k_fused_ldg(FusedArgs a, KeyTab kt, De
             }
             const int64_t ti = task / SPL;
             const int c0 = static_cast<int>(task % SPL) * CH;  // first chunk of this task
-            if (ti < cc.t0) cc.seek(kt, ti);
-            cc.advance_to(kt, ti);
+            if (ti < cc.t0) cc.seek_warp(kt, ti, lane);
+            cc.advance_warp(kt, ti, lane);
             const int64_t j = ti - cc.t0;
             const int64_t e0 = cc.e0 + j * TILE_ELEMS;
             const int64_t w0 = cc.w0 + j * TILE_WORDS;
