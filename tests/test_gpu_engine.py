@@ -40,6 +40,9 @@ CASES = [
     # algo, sizes, k, warmup, iters, alpha, force, bypass
     # > 2 tiles per resident warp: the whole-tile (CH=4) path of the fused kernel
     ("cdsgd", [3_000_000, 4099, 17], 4, 1, 9, 0.5, False, False),
+    # 1,500 keys (some misaligned, some < 1 tile): multi-round warp-collective key seeks and
+    # long cursor jumps between dynamic claims, on the whole-tile path (> 2 tiles per warp)
+    ("cdsgd", [((i * 7919) % 4000) + 1 for i in range(1500)], 4, 1, 9, 0.5, False, False),
     ("cdsgd", [1000, 37, 16, 1], 4, 5, 16, 0.5, False, False),
     ("cdsgd", [300], 3, 0, 12, 0.5, False, False),
     ("cdsgd", [4099, 512, 3], 2, 1, 11, 0.5, False, False),
