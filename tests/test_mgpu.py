@@ -31,3 +31,17 @@ def test_multi_gpu_engine_parity(world):
     res = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
     assert res.returncode == 0, res.stdout[-4000:] + res.stderr[-4000:]
     assert f"MGPU OK world={world}" in res.stdout
+
+
+def test_multi_gpu_push_staging_parity():
+    """The optional push staging of the exact correction (CDSGD_STAGE_PUSH=1: K2 stores each
+    element into its owner's receive row, the reduce reads locally) at N=2."""
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr", "127.0.0.1", "--master-port", str(free_port()),
+           os.path.join(ROOT, "tests", "mgpu_check.py"), "p2p-exact"]
+    env = dict(os.environ, CDSGD_STAGE_PUSH="1")
+    res = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT, env=env)
+    assert res.returncode == 0, res.stdout[-4000:] + res.stderr[-4000:]
+    assert "MGPU OK world=2" in res.stdout
