@@ -52,12 +52,15 @@ __device__ __forceinline__ d4 ld_stream(const double* p) {
         : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w) : "l"(p));
     return v;
 }
+#ifndef CDSGD_ST_HINT
+#define CDSGD_ST_HINT "cs"  // streaming stores (vs L1::no_allocate: -1 us on F and K2 at ResNet-50 size)
+#endif
 __device__ __forceinline__ void st_stream(double* p, double a, double b, double c, double d) {
-    asm volatile("st.global.L1::no_allocate.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(a), "d"(b),
+    asm volatile("st.global." CDSGD_ST_HINT ".v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(a), "d"(b),
                  "d"(c), "d"(d));
 }
 __device__ __forceinline__ void st_stream(float* p, float a, float b, float c, float d) {
-    asm volatile("st.global.L1::no_allocate.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(a), "f"(b),
+    asm volatile("st.global." CDSGD_ST_HINT ".v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(a), "f"(b),
                  "f"(c), "f"(d));
 }
 __device__ __forceinline__ uint32_t ld_word(const uint32_t* p) {
