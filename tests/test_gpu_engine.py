@@ -296,3 +296,30 @@ def test_module_integration_matches_oracle(pkg):
     m.flush()
     W = torch.cat([p.detach().reshape(-1) for p in net.parameters()]).cpu().numpy()
     np.testing.assert_allclose(W, orc.W, rtol=RTOL, atol=ATOL)
+
+
+def test_engine_full_resnet50_vs_c_port(pkg):
+    """The headline workload at FULL size (161 keys, 25,557,032 elements), N=1, k=4: the
+    engine's residual is bitwise the reference round's (C restatement, oracle/cpu_port.py)
+    after every round through two k-periods (fused, local-only, fold paths and every
+    key's partial last tile), compute weights and the final W within rtol 1e-5."""
+    from oracle import cpu_port
+
+    _, E, L, Wk = pkg
+    if cpu_port.load() is None:
+        pytest.skip("C port not built")
+    layout = L.by_name("resnet50")
+    n = layout.total
+    w0 = np.random.default_rng([11, 999]).standard_normal(n).astype(np.float32)
+    hp = E.HyperParams(algo="cdsgd", workers=1, eta_global=0.1, eta_local=0.4, k=4, alpha=0.5, warmup_n=0)
+    wk = Wk.CDSGDWorker(layout, hp, w0)
+    port = cpu_port.CPortEngine(w0.astype(np.float64), [s.length for s in layout.spans], 1, k=4, alpha=0.5)
+    for t in range(9):
+        g = (0.3 * np.random.default_rng([11, t]).standard_normal(n)).astype(np.float32)
+        wk.step(torch.from_numpy(g).cuda())
+        port.step(g[None, :])
+        assert np.array_equal(bits(wk.residual.cpu().numpy()), bits(port.res[0])), f"residual round {t}"
+        np.testing.assert_allclose(wk.compute_weights().cpu().numpy(), port.loc[0], rtol=RTOL, atol=ATOL,
+                                   err_msg=f"compute weights round {t}")
+    wk.flush()
+    np.testing.assert_allclose(wk.weights.cpu().numpy(), port.W, rtol=RTOL, atol=ATOL)
