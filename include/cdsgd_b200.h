@@ -160,6 +160,12 @@ int cdsgd_allreduce_sum_f32(cdsgd_comm* comm, const float* send, float* recv, in
  * paper's compute/communication overlap. Warm-up rounds before warmup_n-1 and
  * the non-local algorithms (ssgd/bitsgd) complete synchronously.
  * cdsgd_engine_flush applies the last pending round (W = W_T).
+ * At N=1 and with the P2P exchange, apply(t-1) and quantize(t) run as ONE kernel that
+ * reads g_t once; at N=1 a correction round is applied inside the preceding apply (its
+ * mean is g_t itself). Engine kernels are launched with programmatic stream
+ * serialization: each waits (griddepcontrol.wait) for its stream predecessor before
+ * touching memory, so caller kernels on `stream` keep plain stream-order semantics.
+ * The grad-norm ring is zeroed by create and then kept zero ahead in-kernel.
  * Buffers are caller-owned device memory (sizes in the struct comments). */
 typedef struct {
     int32_t algo;      /* CDSGD_ALGO_* (engine.py:76) */
@@ -202,7 +208,7 @@ int cdsgd_engine_check(cdsgd_engine* eng, void* stream, int64_t* round, int64_t*
 /* 1 if round `t` (0-based) pushes codes under the engine's schedule (engine.py:345-355). */
 int cdsgd_engine_round_compressed(const cdsgd_engine* eng, int64_t t);
 /* Fused NVLink exchange (replaces the NCCL all-gather of codes on compressed rounds).
- * Every rank allocates one symmetric buffer of cdsgd_p2p_bytes(nranks, words) bytes
+ * Every rank allocates one symmetric buffer of cdsgd_p2p_bytes(nranks, n, words) bytes
  * (zero-filled; e.g. torch symmetric memory), maps all peers' buffers, and passes
  * the nranks base addresses (index = rank, 256-byte aligned) before round 0. K1 then
  * stores each packed word directly into every rank's slot and publishes a release
