@@ -216,7 +216,8 @@ def exchange_desc(exchange: str, world: int) -> str:
         return "none at N=1: codes decoded locally; each correction round folded into the preceding K2"
     codes = ("codes all-gathered inside the quantizing kernel by NVLink stores to peer memory (symmetric memory, "
              "release/acquire flags)" if exchange != "nccl" else "ncclAllGather(packed codes)")
-    corr = ("; exact sharded fp64 NVLink reduce every k-th round" if exchange == "p2p-exact"
+    corr = ("; exact sharded fp64 NVLink reduce every k-th round" if exchange == "p2p-exact" else
+            "; every k-th round an all-reduce split between NCCL and the copy engines" if exchange == "p2p"
             else "; ncclAllReduce(fp32) every k-th round")
     return codes + corr
 
@@ -403,17 +404,26 @@ def run_ours(args):
         n_comp = sum(1 for i in range(K) if wk.round_compressed(W + i))
         n_full = K - n_comp
         nccl_codes = args.exchange == "nccl"
+        cef = wk.ce_fraction  # share of each correction all-reduce on the copy engines (p2p mode)
         exch = {"mode": args.exchange, "code_bytes_per_rank_per_round": P,
                 "code_bus_bytes_per_round": (world - 1) * P,
                 "code_path": "ncclAllGather" if nccl_codes else "NVLink stores inside the quantizing kernel",
                 "correction_bytes": 4 * n,
-                "correction_path": "sharded fp64 NVLink reduce" if args.exchange == "p2p-exact" else "ncclAllReduce"}
+                "correction_path": ("sharded fp64 NVLink reduce" if args.exchange == "p2p-exact" else
+                                    f"ncclAllReduce of {100 * (1 - cef):.0f} % of the elements"
+                                    + (f" + copy-engine reduce-scatter/all-gather of {100 * cef:.0f} %" if cef else ""))}
+        ar_bus = 2 * (world - 1) / world * 4 * n  # nccl-tests bus bytes of one full all-reduce
         if prof["exchange"]["n"]:
             # NCCL calls on the exchange stream: all-gathers (nccl mode) and correction all-reduces
-            bus_bytes = (n_comp * (world - 1) * P if nccl_codes else 0) + n_full * 2 * (world - 1) / world * 4 * n
+            bus_bytes = (n_comp * (world - 1) * P if nccl_codes else 0) + n_full * (1 - cef) * ar_bus
             exch.update({"nccl_calls": prof["exchange"]["n"], "nccl_total_ms": prof["exchange"]["ms"],
                          "nccl_bus_gbs": bus_bytes / (prof["exchange"]["ms"] / 1e3) / 1e9, "nvlink_peak_gbs": 900.0})
             exch["nccl_bus_frac"] = exch["nccl_bus_gbs"] / 900.0
+        if prof["exchange_ce"]["n"]:
+            ce_bytes = n_full * cef * ar_bus
+            exch.update({"ce_calls": prof["exchange_ce"]["n"], "ce_total_ms": prof["exchange_ce"]["ms"],
+                         "ce_bus_gbs": ce_bytes / (prof["exchange_ce"]["ms"] / 1e3) / 1e9})
+            exch["ce_bus_frac"] = exch["ce_bus_gbs"] / 900.0
 
     # ---------------- end-to-end through the public API with host buffers
     e2e = None

@@ -214,7 +214,9 @@ int cdsgd_engine_round_compressed(const cdsgd_engine* eng, int64_t t);
  * stores each packed word directly into every rank's slot and publishes a release
  * flag; K2 acquires all ranks' flags (spin on local memory, ~10 s timeout ->
  * CDSGD_ERR_STATE at cdsgd_engine_check) and releases the slot. Correction rounds
- * use ncclAllReduce on the engine's stream (overlapped with compute) unless
+ * are all-reduced on the engine's streams (overlapped with compute), split between
+ * ncclAllReduce and the copy engines (peer cudaMemcpyAsync reduce-scatter, fp64 shard
+ * sums, all-gather; 30 % of the elements at N=2, 55 % at N>=3) unless
  * exact_correction != 0: then g_t is staged in the symmetric buffer and in the next
  * round every rank reduces its shard of elements from all ranks' stages (fp64,
  * ascending rank — bitwise the reference's sum, engine.py:250-255), applies
@@ -229,12 +231,16 @@ int cdsgd_engine_attach_p2p(cdsgd_engine* eng, void* const* peer_bases, int32_t 
 int cdsgd_engine_join(cdsgd_engine* eng, void* stream);
 /* Per-kernel timing with CUDA events recorded on the launching streams around
  * each K1 / K2 / K3 / local-update launch and each NCCL call, between _begin and
- * _end. _end synchronises and writes 20 doubles, (ms, launches) per class:
+ * _end. _end synchronises and writes 22 doubles, (ms, launches) per class:
  * quantize, apply_quant, apply_full, local_update, exchange (NCCL), fused
  * (apply(t-1) + quantize(t) in one kernel), stage, reduce (P2P correction), wait
- * (P2P correction completion), fused_local (quantize(t) + local update only). */
+ * (P2P correction completion), fused_local (quantize(t) + local update only),
+ * exchange_ce (the copy-engine share of a correction all-reduce). */
 int cdsgd_engine_profile_begin(cdsgd_engine* eng);
-int cdsgd_engine_profile_end(cdsgd_engine* eng, double* out20);
+int cdsgd_engine_profile_end(cdsgd_engine* eng, double* out22);
+/* Fraction of each correction all-reduce moved by the copy engines (P2P mode; 0 = NCCL
+ * only; after cdsgd_engine_attach_p2p). */
+double cdsgd_engine_ce_fraction(const cdsgd_engine* eng);
 
 #ifdef __cplusplus
 }

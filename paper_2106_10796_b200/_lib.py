@@ -84,6 +84,7 @@ _SIGS = {
     "cdsgd_engine_attach_p2p": (C.c_int, [vp, C.POINTER(vp), i32, i32]),
     "cdsgd_engine_profile_begin": (C.c_int, [vp]),
     "cdsgd_engine_profile_end": (C.c_int, [vp, C.POINTER(f64)]),
+    "cdsgd_engine_ce_fraction": (C.c_double, [vp]),
 }
 
 EXPORTED_SYMBOLS = tuple(_SIGS)

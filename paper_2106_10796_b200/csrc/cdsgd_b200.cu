@@ -621,7 +621,8 @@ struct cdsgd_engine {
     cdsgd_engine_desc d{};
     const cdsgd_layout* L = nullptr;
     cdsgd_comm* comm = nullptr;
-    cudaStream_t xs = nullptr;
+    cudaStream_t xs = nullptr, xs2 = nullptr;  // exchange streams (xs2: copy-engine share)
+    cudaEvent_t evC = nullptr;
     cudaEvent_t evQ[2] = {nullptr, nullptr};
     cudaEvent_t evX[2] = {nullptr, nullptr};
     DecodeTab tab{};
@@ -653,6 +654,10 @@ struct cdsgd_engine {
     // faster at N=4 (461 vs 442 Gelem/s): the pushes make K2 NVLink-bound. CDSGD_STAGE_PUSH=1.
     bool stage_push = false;
     int64_t off_W = 0, off_stage[2] = {0, 0}, off_gready = 0, off_gfreed = 0, off_wdone = 0, off_gpart = 0;
+    int64_t off_gsum[2] = {0, 0};
+    // P2P mode: fraction of each correction all-reduce moved by the copy engines
+    // (p2p_ce_allreduce on stream xs2) beside NCCL's share (0 = NCCL only)
+    double ce_frac = 0.0;
     int64_t last_stage[2] = {-1, -1};  // last correction round that used staging slot s
     int64_t ncorr = 0;                 // P2P correction rounds staged so far (slot = ncorr & 1)
     int pend_slot = 0;                 // staging slot of the pending correction round
@@ -665,7 +670,7 @@ struct cdsgd_engine {
     bool diag_no_wait = false;         // timing diagnostic: skip the code-exchange flag waits
     int sc_fence = 0;                  // CDSGD_SC_FENCE=1: fence.sc.sys publish (A/B knob)
     // profiling: event pairs per kernel class (0 quant, 1 apply_q, 2 apply_f, 3 local, 4 exchange, 5 fused,
-    // 6 stage, 7 reduce, 8 wait, 9 fused local-only)
+    // 6 stage, 7 reduce, 8 wait, 9 fused local-only, 10 copy-engine share of a correction all-reduce)
     bool prof = false;
     std::vector<cudaEvent_t> ev_pool;
     size_t ev_used = 0;
@@ -778,10 +783,102 @@ int reduce_ctas() {
     }();
     return v;
 }
-template <int NR>
+template <int NR, bool SUM = false>
 void launch_reduce_t(const ReduceArgs& a, int64_t len, cudaStream_t C) {
-    const int grid = std::min(flat_grid(k_reduce<NR>, (len + 3) / 4), reduce_ctas());
-    launch_pdl(k_reduce<NR>, grid, THREADS, 0, C, a);
+    const int grid = std::min(flat_grid(k_reduce<NR, SUM>, (len + 3) / 4), reduce_ctas());
+    launch_pdl(k_reduce<NR, SUM>, grid, THREADS, 0, C, a);
+}
+
+// Part of a correction round's all-reduce on the COPY ENGINES: elements [off, off + cnt)
+// of g_p. Each owner's slice goes to its receive row by cudaMemcpyAsync (no SMs), each
+// owner sums its shard from local rows (fp64, ascending rank, rounded once to fp32 — the
+// same value on every rank), and the sum shard is copied into every rank's gsum. Flags
+// order the phases. Runs beside ncclAllReduce of [0, off) (split_correction).
+int p2p_ce_allreduce(cdsgd_engine* E, int64_t p, const float* g, cudaStream_t X, int64_t off, int64_t cnt) {
+    const int nr = E->d.nranks, me = E->d.rank;
+    const int s = static_cast<int>(E->ncorr & 1);
+    char* local = E->peer[me];
+    const int64_t ck = (((cnt + nr - 1) / nr) + 3) / 4 * 4;  // shard per owner, <= E->chunk
+    const int64_t m0 = std::min<int64_t>(off + cnt, off + ck * me), m1 = std::min<int64_t>(off + cnt, m0 + ck);
+    P2PArgs fw{};  // 1. flow control: every owner finished reading its row `me` of slot s
+    fw.nranks = nr;
+    fw.wait_flags = at<const uint64_t>(local, E->off_gfreed) + s * nr;
+    fw.wait_value = E->last_stage[s] >= 0 ? static_cast<uint64_t>(E->last_stage[s]) + 1 : 0;
+    fw.err = E->d.err;
+    E->last_stage[s] = p;
+    E->ncorr += 1;
+    if (fw.wait_value != 0) {
+        k_wait_sum<<<1, 32, 0, X>>>(fw, nullptr, 0, nullptr, nullptr, nullptr);
+        LAUNCH_CHECK();
+    }
+    for (int k = 1; k <= nr; ++k) {  // 2. reduce-scatter: my slice of owner o's shard -> o's row `me`
+        const int o = (me + k) % nr;
+        const int64_t o0 = std::min<int64_t>(off + cnt, off + ck * o), o1 = std::min<int64_t>(off + cnt, o0 + ck);
+        if (o1 > o0)
+            CUDA_TRY(cudaMemcpyAsync(at<float>(E->peer[o], E->off_stage[s]) + static_cast<int64_t>(me) * ck, g + o0,
+                                     (o1 - o0) * sizeof(float), cudaMemcpyDeviceToDevice, X));
+    }
+    P2PArgs fr{};
+    fr.nranks = nr;
+    for (int r = 0; r < nr; ++r) fr.publish[r] = at<uint64_t>(E->peer[r], E->off_gready) + s * nr + me;
+    fr.publish_value = static_cast<uint64_t>(p) + 1;
+    k_flags<<<1, 32, 0, X>>>(fr);
+    LAUNCH_CHECK();
+    ReduceArgs a{};  // 3. my shard from the N local rows -> my gsum (fp32 of the fp64 sum)
+    for (int r = 0; r < nr; ++r) {
+        a.stage[r] = at<const float>(local, E->off_stage[s]) + static_cast<int64_t>(r) * ck - m0;
+        a.xa.publish[r] = at<uint64_t>(E->peer[r], E->off_gfreed) + s * nr + me;
+    }
+    a.Wdst[0] = at<float>(local, E->off_gsum[p & 1]);
+    a.ndst = 1;
+    a.s0 = m0;
+    a.s1 = m1;
+    a.nranks = nr;
+    a.xa.nranks = nr;
+    a.xa.wait_flags = at<const uint64_t>(local, E->off_gready) + s * nr;
+    a.xa.wait_value = static_cast<uint64_t>(p) + 1;
+    a.xa.publish_value = static_cast<uint64_t>(p) + 1;
+    a.xa.counter = E->counters + 3;
+    a.xa.sc_fence = E->sc_fence;
+    a.xa.err = E->d.err;
+    if (m1 > m0) {
+        switch (nr) {
+            case 2: launch_reduce_t<2, true>(a, m1 - m0, X); break;
+            case 3: launch_reduce_t<3, true>(a, m1 - m0, X); break;
+            case 4: launch_reduce_t<4, true>(a, m1 - m0, X); break;
+            case 5: launch_reduce_t<5, true>(a, m1 - m0, X); break;
+            case 6: launch_reduce_t<6, true>(a, m1 - m0, X); break;
+            case 7: launch_reduce_t<7, true>(a, m1 - m0, X); break;
+            case 8: launch_reduce_t<8, true>(a, m1 - m0, X); break;
+            default: return fail(CDSGD_ERR_ARG, "P2P correction supports 2..8 ranks");
+        }
+        LAUNCH_CHECK();
+    } else {  // empty shard: still take part in the ready / freed protocol
+        k_wait_sum<<<1, 32, 0, X>>>(a.xa, nullptr, 0, nullptr, nullptr, nullptr);
+        LAUNCH_CHECK();
+        k_flags<<<1, 32, 0, X>>>(a.xa);
+        LAUNCH_CHECK();
+    }
+    for (int k = 1; k < nr && m1 > m0; ++k) {  // 4. all-gather of my sum shard, then wdone[me]
+        const int r = (me + k) % nr;
+        CUDA_TRY(cudaMemcpyAsync(at<float>(E->peer[r], E->off_gsum[p & 1]) + m0,
+                                 at<const float>(local, E->off_gsum[p & 1]) + m0, (m1 - m0) * sizeof(float),
+                                 cudaMemcpyDeviceToDevice, X));
+    }
+    P2PArgs fd{};
+    fd.nranks = nr;
+    for (int r = 0; r < nr; ++r) fd.publish[r] = at<uint64_t>(E->peer[r], E->off_wdone) + me;
+    fd.publish_value = static_cast<uint64_t>(p) + 1;
+    k_flags<<<1, 32, 0, X>>>(fd);
+    LAUNCH_CHECK();
+    P2PArgs w{};  // 5. every rank's shard has landed in my gsum
+    w.nranks = nr;
+    w.wait_flags = at<const uint64_t>(local, E->off_wdone);
+    w.wait_value = static_cast<uint64_t>(p) + 1;
+    w.err = E->d.err;
+    k_wait_sum<<<1, 32, 0, X>>>(w, nullptr, 0, nullptr, nullptr, nullptr);
+    LAUNCH_CHECK();
+    return CDSGD_OK;
 }
 
 // Apply correction round p: reduce my shard from every rank's stage, broadcast W',
@@ -957,6 +1054,8 @@ extern "C" int cdsgd_engine_create(const cdsgd_engine_desc* d, const cdsgd_layou
         int lo = 0, hi = 0;
         cudaDeviceGetStreamPriorityRange(&lo, &hi);
         e = cudaStreamCreateWithPriority(&E->xs, cudaStreamNonBlocking, hi);
+        if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&E->xs2, cudaStreamNonBlocking, hi);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&E->evC, cudaEventDisableTiming);
         for (int i = 0; i < 2 && e == cudaSuccess; ++i) {
             e = cudaEventCreateWithFlags(&E->evQ[i], cudaEventDisableTiming);
             if (e == cudaSuccess) e = cudaEventCreateWithFlags(&E->evX[i], cudaEventDisableTiming);
@@ -975,8 +1074,9 @@ int64_t align256(int64_t v) { return (v + 255) & ~int64_t(255); }
 // Shard owned by each rank in the P2P exact correction: ceil(n/N) rounded up to 4 elements.
 int64_t p2p_chunk(int32_t nranks, int64_t n) { return (((n + nranks - 1) / nranks) + 3) / 4 * 4; }
 // Symmetric buffer: codes slot 0 | slot 1 | ready[2][N] | freed[2][N] | W [n] |
-// recv 0 [N][chunk] | recv 1 [N][chunk] | gready[2][N] | gfreed[2][N] | wdone[N] | gpart[2][N] | end
-void p2p_offsets(int32_t nranks, int64_t n, int64_t words, int64_t* off /* [12] */) {
+// recv 0 [N][chunk] | recv 1 [N][chunk] | gready[2][N] | gfreed[2][N] | wdone[N] | gpart[2][N] |
+// gsum 0 [n] | gsum 1 [n] | end
+void p2p_offsets(int32_t nranks, int64_t n, int64_t words, int64_t* off /* [14] */) {
     const int64_t flags = align256(2 * nranks * 8);
     const int64_t recv = align256(4 * static_cast<int64_t>(nranks) * p2p_chunk(nranks, n));
     off[0] = 0;
@@ -990,18 +1090,20 @@ void p2p_offsets(int32_t nranks, int64_t n, int64_t words, int64_t* off /* [12] 
     off[8] = off[7] + flags;
     off[9] = off[8] + flags;
     off[10] = off[9] + align256(nranks * 8);
-    off[11] = off[10] + flags;
+    off[11] = off[10] + flags;               // gsum 0
+    off[12] = off[11] + align256(4 * n);     // gsum 1
+    off[13] = off[12] + align256(4 * n);     // end
 }
 }  // namespace
 
 extern "C" int64_t cdsgd_p2p_bytes(int32_t nranks, int64_t n, int64_t words) {
-    int64_t off[12];
+    int64_t off[14];
     p2p_offsets(nranks, n, words, off);
-    return off[11];
+    return off[13];
 }
 
 extern "C" int64_t cdsgd_p2p_weights_offset(int32_t nranks, int64_t n, int64_t words) {
-    int64_t off[12];
+    int64_t off[14];
     p2p_offsets(nranks, n, words, off);
     return off[4];
 }
@@ -1017,7 +1119,7 @@ extern "C" int cdsgd_engine_attach_p2p(cdsgd_engine* E, void* const* peer_bases,
             return fail(CDSGD_ERR_ARG, "peer base %d is NULL or not 256-byte aligned", r);
         E->peer[r] = static_cast<char*>(peer_bases[r]);
     }
-    int64_t off[12];
+    int64_t off[14];
     p2p_offsets(nranks, E->L->n, E->L->nwords, off);
     E->off_slot[0] = off[0];
     E->off_slot[1] = off[1];
@@ -1030,7 +1132,12 @@ extern "C" int cdsgd_engine_attach_p2p(cdsgd_engine* E, void* const* peer_bases,
     E->off_gfreed = off[8];
     E->off_wdone = off[9];
     E->off_gpart = off[10];
+    E->off_gsum[0] = off[11];
+    E->off_gsum[1] = off[12];
     char* local = E->peer[E->d.rank];
+    // correction sums land in symmetric memory (the NCCL-free all-reduce stores shards there)
+    E->d.gsum[0] = reinterpret_cast<float*>(local + E->off_gsum[0]);
+    E->d.gsum[1] = reinterpret_cast<float*>(local + E->off_gsum[1]);
     E->d.gathered[0] = reinterpret_cast<uint32_t*>(local + E->off_slot[0]);
     E->d.gathered[1] = reinterpret_cast<uint32_t*>(local + E->off_slot[1]);
     // the W replica moves into symmetric memory (peers store their W' shards into it)
@@ -1058,6 +1165,10 @@ extern "C" int cdsgd_engine_attach_p2p(cdsgd_engine* E, void* const* peer_bases,
         E->diag_local_codes = nr != nullptr && nr[0] == '1';
         const char* nw = getenv("CDSGD_DIAG_NO_WAIT");  // timing diagnostic only: races, wrong results
         E->diag_no_wait = nw != nullptr && nw[0] == '1';
+        // measured best share on B200: 0.3 at N=2 (+4 %), 0.55 at N=4 (+5 %); CDSGD_CE_FRAC overrides
+        const char* cf = getenv("CDSGD_CE_FRAC");
+        const double dflt = nranks == 2 ? 0.3 : 0.55;
+        E->ce_frac = exact_correction ? 0.0 : (cf == nullptr ? dflt : std::min(1.0, std::max(0.0, atof(cf))));
         const char* sp = getenv("CDSGD_STAGE_PUSH");
         E->stage_push = sp != nullptr && sp[0] == '1';
         const char* sf = getenv("CDSGD_SC_FENCE");
@@ -1089,7 +1200,7 @@ extern "C" int cdsgd_engine_profile_begin(cdsgd_engine* E) {
 extern "C" int cdsgd_engine_profile_end(cdsgd_engine* E, double* out) {
     if (E == nullptr || out == nullptr) return fail(CDSGD_ERR_ARG, "NULL argument");
     E->prof = false;
-    for (int i = 0; i < 20; ++i) out[i] = 0.0;
+    for (int i = 0; i < 22; ++i) out[i] = 0.0;
     for (const auto& m : E->prof_marks) {
         CUDA_TRY(cudaEventSynchronize(E->ev_pool[m.second + 1]));
         float ms = 0.f;
@@ -1105,18 +1216,23 @@ extern "C" int cdsgd_engine_profile_end(cdsgd_engine* E, double* out) {
 extern "C" int cdsgd_engine_destroy(cdsgd_engine* E) {
     if (E == nullptr) return CDSGD_OK;
     if (E->xs) cudaStreamSynchronize(E->xs);
+    if (E->xs2) cudaStreamSynchronize(E->xs2);
     for (cudaEvent_t ev : E->ev_pool) cudaEventDestroy(ev);
+    if (E->evC) cudaEventDestroy(E->evC);
     for (int i = 0; i < 2; ++i) {
         if (E->evQ[i]) cudaEventDestroy(E->evQ[i]);
         if (E->evX[i]) cudaEventDestroy(E->evX[i]);
     }
     if (E->xs) cudaStreamDestroy(E->xs);
+    if (E->xs2) cudaStreamDestroy(E->xs2);
     if (E->counters) cudaFree(E->counters);
     if (E->gacc) cudaFree(E->gacc);
     if (E->sched) cudaFree(E->sched);
     delete E;
     return CDSGD_OK;
 }
+
+extern "C" double cdsgd_engine_ce_fraction(const cdsgd_engine* E) { return E != nullptr && E->p2p ? E->ce_frac : 0.0; }
 
 extern "C" int cdsgd_engine_round_compressed(const cdsgd_engine* E, int64_t t) {
     bool c = false;
@@ -1303,7 +1419,28 @@ extern "C" int cdsgd_engine_step(cdsgd_engine* E, const float* g, void* stream) 
     }
     // 2. exchange round t on the engine's stream (codes are already delivered when fused)
     E->xused[t & 1] = nr > 1 && (!E->p2p || (!comp && !E->pcorr));
-    if (E->xused[t & 1]) {
+    if (E->xused[t & 1] && !comp && E->p2p && E->ce_frac > 0.0) {
+        // correction all-reduce split between NCCL (stream X, SMs) and the copy engines
+        // (stream X2): the copy engines barely contend with the compute kernels
+        const int64_t n = E->L->n;
+        const int64_t cnt = std::min<int64_t>(n, static_cast<int64_t>(E->ce_frac * n) / 4 * 4);
+        const int64_t off = n - cnt;
+        CUDA_TRY(cudaEventRecord(E->evQ[t & 1], C));
+        CUDA_TRY(cudaStreamWaitEvent(E->xs, E->evQ[t & 1], 0));
+        CUDA_TRY(cudaStreamWaitEvent(E->xs2, E->evQ[t & 1], 0));
+        const long pi = prof_start(E, 4, E->xs);
+        if (off > 0)
+            NCCL_TRY(ncclAllReduce(g, E->d.gsum[t & 1], static_cast<size_t>(off), ncclFloat, ncclSum, E->comm->nccl,
+                                   E->xs));
+        prof_stop(E, pi, E->xs);
+        const long pc = prof_start(E, 10, E->xs2);
+        rc = p2p_ce_allreduce(E, t, g, E->xs2, off, cnt);
+        if (rc != CDSGD_OK) return rc;
+        prof_stop(E, pc, E->xs2);
+        CUDA_TRY(cudaEventRecord(E->evC, E->xs2));
+        CUDA_TRY(cudaStreamWaitEvent(E->xs, E->evC, 0));
+        CUDA_TRY(cudaEventRecord(E->evX[t & 1], E->xs));
+    } else if (E->xused[t & 1]) {
         CUDA_TRY(cudaEventRecord(E->evQ[t & 1], C));
         CUDA_TRY(cudaStreamWaitEvent(E->xs, E->evQ[t & 1], 0));
         const long pi = prof_start(E, 4, E->xs);

@@ -60,6 +60,7 @@ struct ReduceArgs {
     double* gpart_dst[MAX_RANKS_P2P];   // rank r's gpart[me]
     P2PArgs xa;                         // wait: gready[slot][*] >= t+1; publish: gfreed[slot][me]
     P2PArgs xb;                         // publish: wdone[me]
+    int ndst;                           // destinations written: Wdst[0, ndst) (0 = all NR)
 };
 
 template <int NR>
@@ -72,17 +73,30 @@ __device__ __forceinline__ float reduce_apply1(const float (&g)[NR], float w, do
     return __double2float_rn(__dsub_rn(static_cast<double>(w), __dmul_rn(eta, mean)));  // engine.py:511
 }
 
+// SUM mode (p2p exchange's NCCL-free correction all-reduce): the shard's fp64 ascending
+// sum rounded once to fp32 is stored into every rank's gsum (Wdst), W is not touched and
+// K3 applies it after K2 in stream order — a deterministic all-reduce whose result is
+// bitwise equal on all ranks and at least as accurate as a fp32 ring sum.
 template <int NR>
+__device__ __forceinline__ float sum1(const float (&g)[NR]) {
+    double tot = static_cast<double>(g[0]);
+#pragma unroll
+    for (int r = 1; r < NR; ++r) tot = __dadd_rn(tot, static_cast<double>(g[r]));
+    return __double2float_rn(tot);
+}
+
+template <int NR, bool SUM = false>
 __global__ void __launch_bounds__(256) k_reduce(ReduceArgs a) {
     pdl_enter(nullptr, nullptr);
     p2p_wait(a.xa);
     const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const int64_t nth = (int64_t)gridDim.x * blockDim.x;
     const int64_t len = a.s1 - a.s0;
+    const int nd = a.ndst > 0 ? a.ndst : NR;
     double msq = 0.0;
-    bool vec = aligned_to(a.W + a.s0, 16);
+    bool vec = SUM || aligned_to(a.W + a.s0, 16);
 #pragma unroll
-    for (int r = 0; r < NR; ++r) vec = vec && aligned_to(a.stage[r] + a.s0, 16) && aligned_to(a.Wdst[r] + a.s0, 16);
+    for (int r = 0; r < NR; ++r) vec = vec && aligned_to(a.stage[r] + a.s0, 16) && aligned_to(a.Wdst[r < nd ? r : 0] + a.s0, 16);
     int64_t done = 0;
     if (vec) {
         // U float4 positions per thread per iteration, every (remote) load issued before any use
@@ -97,7 +111,7 @@ __global__ void __launch_bounds__(256) k_reduce(ReduceArgs a) {
                 const int64_t e = a.s0 + 4 * (i + u * nth);
 #pragma unroll
                 for (int r = 0; r < NR; ++r) gv[u][r] = ld_stream(a.stage[r] + e);  // pull: NVLink loads
-                wv[u] = ld_stream(a.W + e);
+                if constexpr (!SUM) wv[u] = ld_stream(a.W + e);
             }
 #pragma unroll
             for (int u = 0; u < U; ++u) {
@@ -108,12 +122,17 @@ __global__ void __launch_bounds__(256) k_reduce(ReduceArgs a) {
                     g0[r] = gv[u][r].x; g1[r] = gv[u][r].y; g2[r] = gv[u][r].z; g3[r] = gv[u][r].w;
                 }
                 float4 o;
-                o.x = reduce_apply1<NR>(g0, wv[u].x, a.eta_g, a.inv_n, msq);
-                o.y = reduce_apply1<NR>(g1, wv[u].y, a.eta_g, a.inv_n, msq);
-                o.z = reduce_apply1<NR>(g2, wv[u].z, a.eta_g, a.inv_n, msq);
-                o.w = reduce_apply1<NR>(g3, wv[u].w, a.eta_g, a.inv_n, msq);
+                if constexpr (SUM) {
+                    o = make_float4(sum1<NR>(g0), sum1<NR>(g1), sum1<NR>(g2), sum1<NR>(g3));
+                } else {
+                    o.x = reduce_apply1<NR>(g0, wv[u].x, a.eta_g, a.inv_n, msq);
+                    o.y = reduce_apply1<NR>(g1, wv[u].y, a.eta_g, a.inv_n, msq);
+                    o.z = reduce_apply1<NR>(g2, wv[u].z, a.eta_g, a.inv_n, msq);
+                    o.w = reduce_apply1<NR>(g3, wv[u].w, a.eta_g, a.inv_n, msq);
+                }
 #pragma unroll
-                for (int r = 0; r < NR; ++r) *reinterpret_cast<float4*>(a.Wdst[r] + e) = o;  // NVLink stores
+                for (int r = 0; r < NR; ++r)
+                    if (r < nd) *reinterpret_cast<float4*>(a.Wdst[r] + e) = o;  // NVLink stores
             }
         }
         for (; i < nv; i += nth) {
@@ -121,17 +140,22 @@ __global__ void __launch_bounds__(256) k_reduce(ReduceArgs a) {
             float4 gv[NR];
 #pragma unroll
             for (int r = 0; r < NR; ++r) gv[r] = ld_stream(a.stage[r] + e);
-            const float4 wv = ld_stream(a.W + e);
             float g0[NR], g1[NR], g2[NR], g3[NR];
 #pragma unroll
             for (int r = 0; r < NR; ++r) { g0[r] = gv[r].x; g1[r] = gv[r].y; g2[r] = gv[r].z; g3[r] = gv[r].w; }
             float4 o;
-            o.x = reduce_apply1<NR>(g0, wv.x, a.eta_g, a.inv_n, msq);
-            o.y = reduce_apply1<NR>(g1, wv.y, a.eta_g, a.inv_n, msq);
-            o.z = reduce_apply1<NR>(g2, wv.z, a.eta_g, a.inv_n, msq);
-            o.w = reduce_apply1<NR>(g3, wv.w, a.eta_g, a.inv_n, msq);
+            if constexpr (SUM) {
+                o = make_float4(sum1<NR>(g0), sum1<NR>(g1), sum1<NR>(g2), sum1<NR>(g3));
+            } else {
+                const float4 wv = ld_stream(a.W + e);
+                o.x = reduce_apply1<NR>(g0, wv.x, a.eta_g, a.inv_n, msq);
+                o.y = reduce_apply1<NR>(g1, wv.y, a.eta_g, a.inv_n, msq);
+                o.z = reduce_apply1<NR>(g2, wv.z, a.eta_g, a.inv_n, msq);
+                o.w = reduce_apply1<NR>(g3, wv.w, a.eta_g, a.inv_n, msq);
+            }
 #pragma unroll
-            for (int r = 0; r < NR; ++r) *reinterpret_cast<float4*>(a.Wdst[r] + e) = o;
+            for (int r = 0; r < NR; ++r)
+                if (r < nd) *reinterpret_cast<float4*>(a.Wdst[r] + e) = o;
         }
         done = 4 * nv;
     }
@@ -140,26 +164,39 @@ __global__ void __launch_bounds__(256) k_reduce(ReduceArgs a) {
         float g[NR];
 #pragma unroll
         for (int r = 0; r < NR; ++r) g[r] = a.stage[r][e];
-        const float o = reduce_apply1<NR>(g, a.W[e], a.eta_g, a.inv_n, msq);
+        const float o = SUM ? sum1<NR>(g) : reduce_apply1<NR>(g, a.W[e], a.eta_g, a.inv_n, msq);
 #pragma unroll
-        for (int r = 0; r < NR; ++r) a.Wdst[r][e] = o;
+        for (int r = 0; r < NR; ++r)
+            if (r < nd) a.Wdst[r][e] = o;
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) msq += __shfl_xor_sync(FULL, msq, o);
-    if ((threadIdx.x & 31) == 0 && msq != 0.0) atomicAdd(a.gacc, msq);
+    if (!SUM && (threadIdx.x & 31) == 0 && msq != 0.0) atomicAdd(a.gacc, msq);
     // last CTA: broadcast the shard's sum(mean^2), then release gfreed and wdone
     __syncthreads();
     if (threadIdx.x == 0) {
         if (grid_arrive_last(a.xa.counter, a.xa.sc_fence != 0)) {
-            const double total = *reinterpret_cast<volatile double*>(a.gacc);
-            *reinterpret_cast<volatile double*>(a.gacc) = 0.0;  // ready for the next correction round
-            for (int r = 0; r < a.nranks; ++r) *reinterpret_cast<volatile double*>(a.gpart_dst[r]) = total;
+            if (!SUM) {
+                const double total = *reinterpret_cast<volatile double*>(a.gacc);
+                *reinterpret_cast<volatile double*>(a.gacc) = 0.0;  // ready for the next correction round
+                for (int r = 0; r < a.nranks; ++r) *reinterpret_cast<volatile double*>(a.gpart_dst[r]) = total;
+            }
             fence_acq_rel_sys();  // orders the gpart stores too
             for (int r = 0; r < a.nranks; ++r) {
                 if (a.xa.publish[r] != nullptr) st_relaxed_sys(a.xa.publish[r], a.xa.publish_value);
                 if (a.xb.publish[r] != nullptr) st_relaxed_sys(a.xb.publish[r], a.xb.publish_value);
             }
         }
+    }
+}
+
+// One thread: release publish_value to every rank's flag cell after everything earlier on
+// this stream (copy-engine transfers included) has completed.
+__global__ void k_flags(P2PArgs x) {
+    if (threadIdx.x == 0) {
+        fence_acq_rel_sys();
+        for (int r = 0; r < x.nranks; ++r)
+            if (x.publish[r] != nullptr) st_relaxed_sys(x.publish[r], x.publish_value);
     }
 }
 

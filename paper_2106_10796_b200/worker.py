@@ -185,6 +185,11 @@ class CDSGDWorker:
         """Weights the next gradient must be computed at (engine.py:335-343)."""
         return self.loc if self.state().compute_is_loc else self.W
 
+    @property
+    def ce_fraction(self) -> float:
+        """Share of each correction all-reduce carried by the copy engines (P2P mode)."""
+        return float(self._lib.cdsgd_engine_ce_fraction(self._eng))
+
     def round_compressed(self, t: int) -> bool:
         r = self._lib.cdsgd_engine_round_compressed(self._eng, int(t))
         if r < 0:
@@ -269,10 +274,10 @@ class CDSGDWorker:
 
     def profile_end(self) -> dict:
         """Per-kernel-class total ms and launch counts since profile_begin()."""
-        out = (C.c_double * 20)()
+        out = (C.c_double * 22)()
         _lib.check(self._lib.cdsgd_engine_profile_end(self._eng, out), "profile_end")
         names = ("quantize", "apply_quant", "apply_full", "local_update", "exchange", "fused", "stage", "reduce",
-                 "wait", "fused_local")
+                 "wait", "fused_local", "exchange_ce")
         return {nm: {"ms": out[2 * i], "n": int(out[2 * i + 1])} for i, nm in enumerate(names)}
 
     def close(self) -> None:
