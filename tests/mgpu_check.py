@@ -39,6 +39,8 @@ CASES = [
     ("bitsgd", [640, 7], 5, 5, 5, 0.5),
     ("lusgd", [640, 7], 5, 2, 6, 0.5),
     ("ssgd", [640, 7], 5, 5, 4, 0.5),
+    # fewer elements than ranks x 4: empty shards in the copy-engine share of the correction
+    ("cdsgd", [5, 3], 2, 0, 6, 0.5),
 ]
 
 
