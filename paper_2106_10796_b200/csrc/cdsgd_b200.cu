@@ -1166,8 +1166,10 @@ extern "C" int cdsgd_engine_attach_p2p(cdsgd_engine* E, void* const* peer_bases,
         const char* nw = getenv("CDSGD_DIAG_NO_WAIT");  // timing diagnostic only: races, wrong results
         E->diag_no_wait = nw != nullptr && nw[0] == '1';
         // measured best share on B200: 0.3 at N=2 (+4 %), 0.55 at N=4 (+5 %); CDSGD_CE_FRAC overrides
+        // below ~8M elements the copy-engine phases' fixed costs (peer copies, flag kernels,
+        // waits) outweigh the contention they save (1M elements: 133 -> 101 Gelem/s at N=4)
         const char* cf = getenv("CDSGD_CE_FRAC");
-        const double dflt = nranks == 2 ? 0.3 : 0.55;
+        const double dflt = E->L->n < (int64_t(1) << 23) ? 0.0 : (nranks == 2 ? 0.3 : 0.55);
         E->ce_frac = exact_correction ? 0.0 : (cf == nullptr ? dflt : std::min(1.0, std::max(0.0, atof(cf))));
         const char* sp = getenv("CDSGD_STAGE_PUSH");
         E->stage_push = sp != nullptr && sp[0] == '1';

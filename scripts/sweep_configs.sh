@@ -19,7 +19,7 @@ ks=" ".join(f"{k}={v['avg_us']:.0f}us/{v['frac']:.2f}" for k,v in d["kernels"].i
 print(f"N={sys.argv[1]} {sys.argv[2]:18s} k={sys.argv[3]} value={d['value']:8.1f} Gelem/s step={d['ms_per_step']*1e3:9.1f}us {ks}")
 PY
 }
-for W in single:65536 single:262144 single:1048576 single:4194304 single:16777216 single:67108864 single:268435456 single:1073741824 resnet20 resnet50 vgg16; do run 1 $W 4; done
+[ -z "$SKIP_N1" ] && for W in single:65536 single:262144 single:1048576 single:4194304 single:16777216 single:67108864 single:268435456 single:1073741824 resnet20 resnet50 vgg16; do run 1 $W 4; done
 for N in 2 4; do
   [ $N -gt $NG ] && break
   for K in 2 4 8; do run $N vgg16 $K; done
