@@ -45,3 +45,18 @@ def test_multi_gpu_push_staging_parity():
     res = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT, env=env)
     assert res.returncode == 0, res.stdout[-4000:] + res.stderr[-4000:]
     assert "MGPU OK world=2" in res.stdout
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_multi_gpu_copy_engine_correction_parity(world):
+    """The p2p exchange with the copy-engine share of the correction all-reduce forced on
+    (by default it starts at 8M elements, above these test layouts)."""
+    if torch.cuda.device_count() < world:
+        pytest.skip(f"needs {world} GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr", "127.0.0.1", "--master-port", str(free_port()),
+           os.path.join(ROOT, "tests", "mgpu_check.py"), "p2p"]
+    env = dict(os.environ, CDSGD_CE_FRAC="0.5")
+    res = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT, env=env)
+    assert res.returncode == 0, res.stdout[-4000:] + res.stderr[-4000:]
+    assert f"MGPU OK world={world}" in res.stdout
