@@ -216,7 +216,8 @@ int cdsgd_engine_round_compressed(const cdsgd_engine* eng, int64_t t);
  * CDSGD_ERR_STATE at cdsgd_engine_check) and releases the slot. Correction rounds
  * are all-reduced on the engine's streams (overlapped with compute), split between
  * ncclAllReduce and the copy engines (peer cudaMemcpyAsync reduce-scatter, fp64 shard
- * sums, all-gather; 30 % of the elements at N=2, 55 % at N>=3, from 8M elements) unless
+ * sums, all-gather; 30 % of the elements at N=2, 55 % at N>=3, from 8M elements, on
+ * rounds whose all-reduce overlaps compute) unless
  * exact_correction != 0: then g_t is staged in the symmetric buffer and in the next
  * round every rank reduces its shard of elements from all ranks' stages (fp64,
  * ascending rank — bitwise the reference's sum, engine.py:250-255), applies

@@ -1421,7 +1421,9 @@ extern "C" int cdsgd_engine_step(cdsgd_engine* E, const float* g, void* stream) 
     }
     // 2. exchange round t on the engine's stream (codes are already delivered when fused)
     E->xused[t & 1] = nr > 1 && (!E->p2p || (!comp && !E->pcorr));
-    if (E->xused[t & 1] && !comp && E->p2p && E->ce_frac > 0.0) {
+    // the split pays only when the all-reduce overlaps compute: a synchronous round (ssgd,
+    // warm-up) waits for it at once, and NCCL alone is faster there (ssgd N=4: 0.57 vs 0.69 ms)
+    if (E->xused[t & 1] && !comp && E->p2p && E->ce_frac > 0.0 && !sync_path0) {
         // correction all-reduce split between NCCL (stream X, SMs) and the copy engines
         // (stream X2): the copy engines barely contend with the compute kernels
         const int64_t n = E->L->n;
