@@ -42,6 +42,7 @@ extern "C" {
 #define CDSGD_ERR_STATE -4   /* engine used out of order (maps to SchedulingError) */
 #define CDSGD_ERR_NUMERIC -5 /* a step hit a non-finite accumulator (CodecNumericError) */
 #define CDSGD_ERR_CORRUPT -6 /* reserved symbol 11 in a payload (CorruptPayloadError) */
+#define CDSGD_ERR_PEER -7    /* another rank failed (its flags arrived poisoned); nothing was applied after it */
 
 #define CDSGD_NO_ERROR 0xFFFFFFFFFFFFFFFFull
 #define CDSGD_INDEX_BITS 40 /* err word = (step_tag << 40) | flat element index */
@@ -84,8 +85,10 @@ int cdsgd_layout_offsets(const cdsgd_layout* layout, int64_t* elem_off, int64_t*
  *   r_out = acc - emitted ; 2-bit codes packed 16/word LE, zero pad per key.
  * `grad` is fp32 (grad_dtype CDSGD_F32) or fp64 (CDSGD_F64). r_in may equal r_out.
  * Non-finite acc: atomicMin(err, err_tag | flat index); the caller must then keep
- * r_in (no-mutation-on-error, codec.py:181-185). If *err != CDSGD_NO_ERROR at
- * launch the kernel does nothing (sticky abort). */
+ * r_in (no-mutation-on-error, codec.py:181-185). If *err < err_tag at launch (an
+ * error recorded by an EARLIER round, whose tag is smaller) the kernel does nothing
+ * (sticky abort); an error of the same tag never stops the scan, so the reported
+ * index is the first non-finite element. */
 int cdsgd_quantize(const cdsgd_layout* layout, const void* grad, int32_t grad_dtype,
                    const double* r_in, double* r_out, uint32_t* words, double alpha,
                    uint64_t* err, uint64_t err_tag, void* stream);
@@ -133,6 +136,20 @@ int cdsgd_apply_quant(const cdsgd_layout* layout, float* weights, const uint32_t
 int cdsgd_apply_full(float* weights, const float* gsum, int32_t nranks, int64_t n, double eta_g,
                      const float* g_next, float* loc_out, double eta_l, const uint64_t* err,
                      uint64_t skip_below, double* gnorm_sq, void* stream);
+
+/* One round of the step in ONE pass over g_t (the kernel the engine runs on compressed
+ * rounds): quantize(t) as cdsgd_quantize (codes to `words`, residual r_in -> r_out, err as
+ * there, err_tag = this round's tag) fused with the apply of round t-1 — the decode +
+ * ascending-worker sum of `gathered` (nranks payloads, rank stride rank_stride_words),
+ * W -= eta_g*mean and loc = W' - eta_l*g_t (engine.py:249-255, 385-392, 509-511) — so g_t
+ * is read once for both. gathered == NULL: nothing to apply, only loc = W - eta_l*g_t.
+ * The apply part is skipped if *err < skip_below. nranks <= 8. Decode as K2 (exact table
+ * when every j*alpha is representable, else the sequential fp64 sum). gnorm_sq: += the
+ * round t-1 mean's sum of squares (nullable). */
+int cdsgd_fused_round(const cdsgd_layout* layout, const float* grad, const double* r_in, double* r_out,
+                      uint32_t* words, double alpha, uint64_t* err, uint64_t err_tag, float* weights,
+                      float* loc, const uint32_t* gathered, int32_t nranks, int64_t rank_stride_words,
+                      double eta_g, double eta_l, uint64_t skip_below, double* gnorm_sq, void* stream);
 
 /* ------------------------------------------------------------------ exchange (NCCL)
  * Replaces the PS message passing of _run_lockstep (engine.py:627-661) /

@@ -15,7 +15,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("CDSGD_LIB") or os.path.join(_HERE, "libcdsgd_b200.so")
 
 OK = 0
-ERR_ARG, ERR_CUDA, ERR_NCCL, ERR_STATE, ERR_NUMERIC, ERR_CORRUPT = -1, -2, -3, -4, -5, -6
+ERR_ARG, ERR_CUDA, ERR_NCCL, ERR_STATE, ERR_NUMERIC, ERR_CORRUPT, ERR_PEER = -1, -2, -3, -4, -5, -6, -7
 NO_ERROR = 0xFFFFFFFFFFFFFFFF
 INDEX_BITS = 40
 F32, F64 = 0, 1
@@ -66,6 +66,7 @@ _SIGS = {
     "cdsgd_local_update": (C.c_int, [vp, i32, vp, i32, vp, i32, i64, f64, vp]),
     "cdsgd_apply_quant": (C.c_int, [vp, vp, vp, i32, i64, f64, f64, vp, vp, f64, vp, u64, vp, vp]),
     "cdsgd_apply_full": (C.c_int, [vp, vp, i32, i64, f64, vp, vp, f64, vp, u64, vp, vp]),
+    "cdsgd_fused_round": (C.c_int, [vp, vp, vp, vp, vp, f64, vp, u64, vp, vp, vp, i32, i64, f64, f64, u64, vp, vp]),
     "cdsgd_comm_unique_id": (C.c_int, [vp]),
     "cdsgd_comm_init": (C.c_int, [vp, i32, i32, C.POINTER(vp)]),
     "cdsgd_comm_destroy": (C.c_int, [vp]),
@@ -98,6 +99,11 @@ class LibraryError(RuntimeError):
     def __init__(self, message: str, code: int = ERR_CUDA):
         super().__init__(message)
         self.code = code
+
+
+class PeerFailedError(LibraryError):
+    """Another rank of the exchange failed (its flags arrived poisoned); this rank applied
+    nothing after that round. The failing rank raises the cause (e.g. CodecNumericError)."""
 
 
 def load(path: str = LIB_PATH):

@@ -40,7 +40,8 @@ def sources():
 
 
 def deps():
-    return sources() + [os.path.join(CSRC, "kernels.cuh"), os.path.join(CSRC, "kernels_tma.cuh"), os.path.join(CSRC, "kernels_fused.cuh"), os.path.join(INCLUDE, "cdsgd_b200.h")]
+    # every header of csrc/ (a missing one here means a stale .so after editing it)
+    return sources() + sorted(glob.glob(os.path.join(CSRC, "*.cuh"))) + [os.path.join(INCLUDE, "cdsgd_b200.h")]
 
 
 def up_to_date() -> bool:

@@ -377,9 +377,25 @@ def dequantize(payload: QuantizedPayload) -> torch.Tensor:
 
 
 def dequantize_sum(payloads: Sequence[QuantizedPayload]) -> torch.Tensor:
-    """Ascending-order decode-sum / len(payloads) in fp64 (engine.py:249-255, quantized branch)."""
+    """Ascending-order decode-sum / len(payloads) in fp64 (engine.py:249-255, quantized branch).
+
+    Every payload is decoded with its OWN threshold, as the reference does (dequantize per
+    contribution, engine.py:251): equal thresholds take the single fused kernel, mixed ones
+    decode payload by payload and add in ascending order (the same fp64 operations).
+    Payloads of different lengths cannot be summed (the reference server rejects them,
+    engine.py:500-504): CodecError."""
+    if not payloads:
+        raise CodecError("need at least one payload")
     n = payloads[0].length
+    if any(p.length != n for p in payloads):
+        raise CodecError(f"payload lengths differ: {[p.length for p in payloads]}")
     thr = payloads[0].threshold
+    if any(p.threshold != thr for p in payloads):
+        total = None
+        for p in payloads:
+            d = dequantize(p)
+            total = d if total is None else total + d
+        return total / len(payloads)
     stacked = torch.stack([_device_tensor(p.words).view(torch.int32) for p in payloads]).view(torch.uint32)
     out = torch.empty(n, dtype=torch.float64, device=stacked.device)
     if n == 0:

@@ -114,6 +114,18 @@ bool pdl_on() {
     }();
     return v;
 }
+// Set while enqueueing an apply right after a correction all-reduce was issued on the
+// exchange stream: a PDL launch would make the apply's CTAs resident (spinning in
+// griddepcontrol.wait) while the previous kernel drains, so they hold every SM when the
+// all-reduce becomes eligible and NCCL's kernel starts only once the apply retires
+// (measured at N=2: ~90 us late per correction). A plain launch lets the high-priority
+// exchange stream's CTAs in first.
+thread_local bool tl_plain_launch = false;
+struct PlainLaunchScope {
+    bool prev;
+    explicit PlainLaunchScope(bool on) : prev(tl_plain_launch) { tl_plain_launch = on || prev; }
+    ~PlainLaunchScope() { tl_plain_launch = prev; }
+};
 template <typename... P, typename... A>
 void launch_pdl(void (*kernel)(P...), int grid, int block, size_t smem, cudaStream_t st, A&&... args) {
     cudaLaunchConfig_t cfg = {};
@@ -125,7 +137,7 @@ void launch_pdl(void (*kernel)(P...), int grid, int block, size_t smem, cudaStre
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = pdl_on() ? 1 : 0;
+    cfg.numAttrs = (pdl_on() && !tl_plain_launch) ? 1 : 0;
     (void)cudaLaunchKernelEx(&cfg, kernel, std::forward<A>(args)...);  // errors: cudaGetLastError
 }
 
@@ -553,6 +565,42 @@ extern "C" int cdsgd_apply_full(float* W, const float* gsum, int32_t nr, int64_t
     return launch_apply_full(W, gsum, nr, n, eta_g, gnext, loc, eta_l, err, skip_below, gnorm, S(stream));
 }
 
+extern "C" int cdsgd_fused_round(const cdsgd_layout* L, const float* grad, const double* r_in, double* r_out,
+                                 uint32_t* words, double alpha, uint64_t* err, uint64_t err_tag, float* W,
+                                 float* loc, const uint32_t* gathered, int32_t nr, int64_t stride, double eta_g,
+                                 double eta_l, uint64_t skip_below, double* gnorm, void* stream) {
+    if (L == nullptr) return fail(CDSGD_ERR_ARG, "layout is NULL");
+    if (!(alpha > 0.0)) return fail(CDSGD_ERR_ARG, "threshold alpha must be > 0");
+    if (eta_g < 0 || eta_l < 0) return fail(CDSGD_ERR_ARG, "learning rates must be >= 0");
+    if (nr < 1 || nr > MAX_RANKS_P2P) return fail(CDSGD_ERR_ARG, "nranks must be in [1, %d]", MAX_RANKS_P2P);
+    if (L->n == 0) return CDSGD_OK;
+    if (!grad || !r_in || !r_out || !words || !W || !loc) return fail(CDSGD_ERR_ARG, "NULL buffer");
+    FusedArgs a{};
+    a.g = grad;
+    a.r_in = r_in;
+    a.r_out = r_out;
+    a.words = words;
+    a.alpha = alpha;
+    a.tag = err_tag;
+    a.W = W;
+    a.loc = loc;
+    a.gathered = gathered;
+    a.stride = stride;
+    a.scale = static_cast<float>(eta_g / nr);
+    a.inv_n = 1.0 / nr;
+    a.eta_l = static_cast<float>(eta_l);
+    a.exact = alpha_exact(alpha, nr) ? 1 : 0;
+    a.eta_g_d = eta_g;
+    a.inv_n_or_zero = pow2(nr) ? 1.0 / nr : 0.0;
+    a.skip_below = skip_below;
+    a.gnorm = gathered != nullptr ? gnorm : nullptr;
+    a.err = err;
+    a.sched = nullptr;  // static tile ranges: no scheduler state shared between callers
+    DecodeTab tab;
+    build_tab(tab, alpha, eta_g, nr);
+    return launch_fused(nr, gathered != nullptr ? APPLY_Q : APPLY_L, a, L->tab(), tab, S(stream));
+}
+
 // ------------------------------------------------------------------ NCCL exchange
 struct cdsgd_comm {
     ncclComm_t nccl = nullptr;
@@ -666,6 +714,7 @@ struct cdsgd_engine {
     unsigned int* sched = nullptr;     // [4] dynamic tile schedulers: fused kernel [0,1], K2 [2,3]
     bool fuse = false;                 // apply(t-1) + quantize(t) in one kernel (N=1 or P2P)
     bool pcorr = false;                // P2P mode: correction rounds by the exact sharded NVLink reduce
+    bool plain_after_ar = false;       // plain (non-PDL) launch of the apply beside a correction all-reduce
     bool diag_local_codes = false;     // timing diagnostic: store codes only locally
     bool diag_no_wait = false;         // timing diagnostic: skip the code-exchange flag waits
     int sc_fence = 0;                  // CDSGD_SC_FENCE=1: fence.sc.sys publish (A/B knob)
@@ -811,8 +860,8 @@ int p2p_ce_allreduce(cdsgd_engine* E, int64_t p, const float* g, cudaStream_t X,
         k_wait_sum<<<1, 32, 0, X>>>(fw, nullptr, 0, nullptr, nullptr, nullptr);
         LAUNCH_CHECK();
     }
-    for (int k = 1; k <= nr; ++k) {  // 2. reduce-scatter: my slice of owner o's shard -> o's row `me`
-        const int o = (me + k) % nr;
+    for (int k = 1; k < nr; ++k) {  // 2. reduce-scatter: my slice of owner o's shard -> o's row `me`
+        const int o = (me + k) % nr;   // (my own slice is read in place from g: no local copy)
         const int64_t o0 = std::min<int64_t>(off + cnt, off + ck * o), o1 = std::min<int64_t>(off + cnt, o0 + ck);
         if (o1 > o0)
             CUDA_TRY(cudaMemcpyAsync(at<float>(E->peer[o], E->off_stage[s]) + static_cast<int64_t>(me) * ck, g + o0,
@@ -826,7 +875,7 @@ int p2p_ce_allreduce(cdsgd_engine* E, int64_t p, const float* g, cudaStream_t X,
     LAUNCH_CHECK();
     ReduceArgs a{};  // 3. my shard from the N local rows -> my gsum (fp32 of the fp64 sum)
     for (int r = 0; r < nr; ++r) {
-        a.stage[r] = at<const float>(local, E->off_stage[s]) + static_cast<int64_t>(r) * ck - m0;
+        a.stage[r] = r == me ? g : at<const float>(local, E->off_stage[s]) + static_cast<int64_t>(r) * ck - m0;
         a.xa.publish[r] = at<uint64_t>(E->peer[r], E->off_gfreed) + s * nr + me;
     }
     a.Wdst[0] = at<float>(local, E->off_gsum[p & 1]);
@@ -1040,6 +1089,10 @@ extern "C" int cdsgd_engine_create(const cdsgd_engine_desc* d, const cdsgd_layou
     {
         const char* nf = getenv("CDSGD_NO_FUSE");
         E->fuse = d->nranks == 1 && !(nf != nullptr && nf[0] == '1');
+        // A/B knob: plain launch of the apply beside a correction all-reduce (measured no gain at
+        // N=2: 296 vs 301 Gelem/s — the apply's CTAs fill every SM either way)
+        const char* pa = getenv("CDSGD_PLAIN_AFTER_AR");
+        E->plain_after_ar = pa != nullptr && pa[0] == '1';
         const char* ns = getenv("CDSGD_STATIC_SCHED");
         if (!(ns != nullptr && ns[0] == '1')) {
             if (cudaMalloc(&E->sched, 4 * sizeof(unsigned int)) != cudaSuccess ||
@@ -1329,6 +1382,9 @@ extern "C" int cdsgd_engine_step(cdsgd_engine* E, const float* g, void* stream) 
         a.scale = static_cast<float>(E->d.eta_global / nr);
         a.inv_n = 1.0 / nr;
         a.eta_l = static_cast<float>(E->d.eta_local);
+        a.exact = E->exact;
+        a.eta_g_d = E->d.eta_global;
+        a.inv_n_or_zero = pow2(nr) ? 1.0 / nr : 0.0;
         const int64_t rel = pnd - E->err_base + 1;
         a.skip_below = rel <= 0 ? 0ull : (static_cast<uint64_t>(rel) << CDSGD_INDEX_BITS);
         a.err = E->d.err;
@@ -1458,6 +1514,7 @@ extern "C" int cdsgd_engine_step(cdsgd_engine* E, const float* g, void* stream) 
         CUDA_TRY(cudaEventRecord(E->evX[t & 1], E->xs));
     }
     // 3. apply
+    const PlainLaunchScope plain(E->xused[t & 1] && !comp && E->plain_after_ar);
     const bool sync_path = !E->uses_local || t < E->n_warmup - 1;
     if (sync_path) {
         if (E->pending) return fail(CDSGD_ERR_STATE, "internal: pending round on the synchronous path");
@@ -1561,6 +1618,10 @@ extern "C" int cdsgd_engine_check(cdsgd_engine* E, void* stream, int64_t* round,
     if (h[1] == EXCHANGE_TIMEOUT) {
         E->failed = true;
         return fail(CDSGD_ERR_STATE, "fused exchange timed out waiting for a peer (lost rank?)");
+    }
+    if (h[1] == PEER_FAILED) {
+        E->failed = true;
+        return fail(CDSGD_ERR_PEER, "a peer rank failed (numeric error); this rank stopped applying rounds");
     }
     if (h[1] != NO_ERR) {
         if (index) *index = static_cast<int64_t>(h[1]);

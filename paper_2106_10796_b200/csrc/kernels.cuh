@@ -251,23 +251,42 @@ __device__ __forceinline__ void st_release_sys(uint64_t* p, uint64_t v) {
     asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
-// Block-wide: thread 0 waits until every wait_flags[r] >= wait_value, then all threads proceed.
-__device__ __forceinline__ void p2p_wait(const P2PArgs& x) {
-    if (x.nranks > 0 && x.wait_flags != nullptr && x.wait_value != 0) {
-        if (threadIdx.x == 0) {
-            const long long t0 = clock64();
-            for (int r = 0; r < x.nranks; ++r) {
-                while (ld_acquire_sys(x.wait_flags + r) < x.wait_value) {
-                    __nanosleep(64);
-                    if (clock64() - t0 > (20ll << 30)) {  // ~10 s at 2 GHz
-                        if (x.err) atomicExch(reinterpret_cast<unsigned long long*>(x.err + 1), EXCHANGE_TIMEOUT);
-                        break;
-                    }
-                }
+// Failure propagation: a rank whose error word is set (numeric error of any round, peer
+// failure, timeout) publishes its flags with POISON set. Waiters treat a poisoned flag as
+// arrived (no hang), record PEER_FAILED in their err[1] and skip the apply / quantize, so no
+// replica applies stale or garbage codes after a rank failed — the reference aborts every
+// worker at the failing round. cdsgd_engine_check reports it (CDSGD_ERR_PEER).
+constexpr uint64_t POISON = 1ull << 62;
+constexpr uint64_t PEER_FAILED = 0xFFFFFFFFFFFFFFFDull;
+
+// Thread 0: wait until every wait_flags[r] >= wait_value (timeout -> EXCHANGE_TIMEOUT);
+// returns true if some flag carries POISON.
+__device__ __forceinline__ bool p2p_wait_t0(const P2PArgs& x, long long t0) {
+    bool poisoned = false;
+    if (x.nranks <= 0 || x.wait_flags == nullptr || x.wait_value == 0) return false;
+    for (int r = 0; r < x.nranks; ++r) {
+        uint64_t f;
+        while ((f = ld_acquire_sys(x.wait_flags + r)) < x.wait_value) {
+            __nanosleep(64);
+            if (clock64() - t0 > (20ll << 30)) {  // ~10 s at 2 GHz
+                if (x.err) atomicExch(reinterpret_cast<unsigned long long*>(x.err + 1), EXCHANGE_TIMEOUT);
+                break;
             }
         }
-        __syncthreads();
+        poisoned |= (f & POISON) != 0;
     }
+    if (poisoned && x.err)
+        atomicMin(reinterpret_cast<unsigned long long*>(x.err + 1), static_cast<unsigned long long>(PEER_FAILED));
+    return poisoned;
+}
+
+// Block-wide wait; true (in every thread) if a peer published a poisoned flag.
+__device__ __forceinline__ bool p2p_wait(const P2PArgs& x) {
+    __shared__ int s_poison;
+    if (!(x.nranks > 0 && x.wait_flags != nullptr && x.wait_value != 0)) return false;
+    if (threadIdx.x == 0) s_poison = p2p_wait_t0(x, clock64()) ? 1 : 0;
+    __syncthreads();
+    return s_poison != 0;
 }
 
 __device__ __forceinline__ unsigned atom_add_acq_rel_sys(unsigned int* p, unsigned v) {
@@ -294,6 +313,14 @@ __device__ __forceinline__ bool grid_arrive_last(unsigned int* counter, bool sc_
     return true;
 }
 
+// Value the last CTA publishes: POISON set if this rank has recorded any error (its own
+// numeric error, reserved symbol, timeout or a peer failure) by the end of the launch.
+__device__ __forceinline__ uint64_t publish_word(const P2PArgs& x) {
+    if (x.err == nullptr) return x.publish_value;
+    const volatile uint64_t* e = reinterpret_cast<const volatile uint64_t*>(x.err);
+    return (e[0] != NO_ERR || e[1] != NO_ERR) ? (x.publish_value | POISON) : x.publish_value;
+}
+
 // Block-wide epilogue: the last CTA to finish publishes publish_value to every peer.
 __device__ __forceinline__ void p2p_publish(const P2PArgs& x) {
     if (x.nranks <= 0) return;
@@ -301,31 +328,24 @@ __device__ __forceinline__ void p2p_publish(const P2PArgs& x) {
     if (threadIdx.x == 0) {
         if (grid_arrive_last(x.counter, x.sc_fence != 0)) {
             fence_acq_rel_sys();
+            const uint64_t v = publish_word(x);
             for (int r = 0; r < x.nranks; ++r)
-                if (x.publish[r] != nullptr) st_relaxed_sys(x.publish[r], x.publish_value);
+                if (x.publish[r] != nullptr) st_relaxed_sys(x.publish[r], v);
         }
     }
 }
 
-__device__ __forceinline__ void p2p_wait2(const P2PArgs& a, const P2PArgs& b) {
-    // one barrier for both waits (each waits only if armed)
+// One barrier for both waits (each waits only if armed); true if a peer is poisoned.
+__device__ __forceinline__ bool p2p_wait2(const P2PArgs& a, const P2PArgs& b) {
+    __shared__ int s_poison2;
     if (threadIdx.x == 0) {
-        const P2PArgs* xs[2] = {&a, &b};
         const long long t0 = clock64();
-        for (int i = 0; i < 2; ++i) {
-            const P2PArgs& x = *xs[i];
-            if (x.nranks <= 0 || x.wait_flags == nullptr || x.wait_value == 0) continue;
-            for (int r = 0; r < x.nranks; ++r)
-                while (ld_acquire_sys(x.wait_flags + r) < x.wait_value) {
-                    __nanosleep(64);
-                    if (clock64() - t0 > (20ll << 30)) {
-                        if (x.err) atomicExch(reinterpret_cast<unsigned long long*>(x.err + 1), EXCHANGE_TIMEOUT);
-                        break;
-                    }
-                }
-        }
+        const bool pa = p2p_wait_t0(a, t0);
+        const bool pb = p2p_wait_t0(b, t0);
+        s_poison2 = (pa || pb) ? 1 : 0;
     }
     __syncthreads();
+    return s_poison2 != 0;
 }
 
 __device__ __forceinline__ void p2p_publish2(const P2PArgs& a, const P2PArgs& b, unsigned int* counter) {
@@ -335,9 +355,11 @@ __device__ __forceinline__ void p2p_publish2(const P2PArgs& a, const P2PArgs& b,
         if (grid_arrive_last(counter, (a.nranks > 0 ? a.sc_fence : b.sc_fence) != 0)) {
             const P2PArgs* xs[2] = {&a, &b};
             fence_acq_rel_sys();
-            for (int i = 0; i < 2; ++i)
+            for (int i = 0; i < 2; ++i) {
+                const uint64_t v = publish_word(*xs[i]);
                 for (int r = 0; r < xs[i]->nranks; ++r)
-                    if (xs[i]->publish[r] != nullptr) st_relaxed_sys(xs[i]->publish[r], xs[i]->publish_value);
+                    if (xs[i]->publish[r] != nullptr) st_relaxed_sys(xs[i]->publish[r], v);
+            }
         }
     }
 }
@@ -540,8 +562,8 @@ template <int NR>  // NR > 0: compile-time rank count; NR == 0: runtime (generic
 #endif
 __global__ void __launch_bounds__(256, CDSGD_K2_MINB) k_apply_quant(ApplyQArgs a, KeyTab kt, DecodeTab tab) {
     pdl_enter(a.gclear[0], a.gclear[1]);
-    p2p_wait2(a.x, a.xs);
-    const bool skip = a.err != nullptr && *reinterpret_cast<volatile uint64_t*>(a.err) < a.skip_below;
+    const bool peer_failed = p2p_wait2(a.x, a.xs);
+    const bool skip = peer_failed || (a.err != nullptr && *reinterpret_cast<volatile uint64_t*>(a.err) < a.skip_below);
     __shared__ double s_mean[2 * MAX_RANKS + 1];
     __shared__ float s_upd[2 * MAX_RANKS + 1];
     const int nr = NR > 0 ? NR : a.nranks;

@@ -37,6 +37,12 @@ struct FusedArgs {
     float scale;               // APPLY_F: (float)(eta_g / N)
     double inv_n;
     float eta_l;
+    // APPLY_Q decode: exact = every partial sum j*alpha (|j| <= N) representable, so the
+    // SWAR count + table is bitwise the ascending fp64 sum; otherwise (e.g. alpha = 0.3 at
+    // N >= 3) the tile takes the per-element path with the sequential sum of
+    // engine.py:250-255 (inv_n_or_zero = 1/N for power-of-two N, else 0: divide).
+    int exact;
+    double eta_g_d, inv_n_or_zero;
     uint64_t skip_below;
     double* gnorm;
     uint64_t* err;
@@ -166,10 +172,13 @@ __global__ void __launch_bounds__(256, 2) k_fused_ldg(FusedArgs a, KeyTab kt, De
     constexpr int SPL = CHUNKS / CH;  // tasks per tile
     __shared__ float s_upd[2 * MAX_RANKS + 1];
     pdl_enter(a.gclear[0], a.gclear[1]);
-    p2p_wait2(a.xq, a.xa);
+    const bool peer_failed = p2p_wait2(a.xq, a.xa);
     const uint64_t e0v = a.err != nullptr ? *reinterpret_cast<volatile uint64_t*>(a.err) : ~0ull;
-    const bool q_off = e0v != NO_ERR;
-    const bool a_off = e0v < a.skip_below;
+    // sticky abort: only an error of an EARLIER round (smaller tag) stops the quantize, so a
+    // non-finite value found by one CTA never suppresses the scan of the others in this launch
+    // (the reported index stays the first non-finite element, codec.py:182-185)
+    const bool q_off = e0v < a.tag || peer_failed;
+    const bool a_off = e0v < a.skip_below || peer_failed;
     if (APPLY == APPLY_Q && threadIdx.x < 2 * NR + 1) s_upd[threadIdx.x] = tab.upd[threadIdx.x];
     __syncthreads();
     const int lane = threadIdx.x & 31;
@@ -227,7 +236,7 @@ __global__ void __launch_bounds__(256, 2) k_fused_ldg(FusedArgs a, KeyTab kt, De
             const int nw = nw64 < TILE_WORDS ? static_cast<int>(nw64) : TILE_WORDS;
             const bool fast = aligned_to(a.g + e0, 16) && aligned_to(a.r_in + e0, 32) &&
                               aligned_to(a.r_out + e0, 32) && aligned_to(a.W + e0, 16) && aligned_to(a.loc + e0, 16) &&
-                              (APPLY != APPLY_F || aligned_to(a.gsum + e0, 16));
+                              (APPLY != APPLY_F || aligned_to(a.gsum + e0, 16)) && (APPLY != APPLY_Q || a.exact);
             if (!fast && c0 != 0) continue;  // misaligned tiles: one task does the whole tile
             uint32_t myword = 0;
             if (fast) {
@@ -244,10 +253,12 @@ __global__ void __launch_bounds__(256, 2) k_fused_ldg(FusedArgs a, KeyTab kt, De
                     const int el = 32 * s + lane;
                     int cn = 0;
                     bool rsv = false;
+                    uint32_t cds[APPLY == APPLY_Q ? NR : 1];
                     if constexpr (APPLY == APPLY_Q) {
 #pragma unroll
                         for (int r = 0; r < NR; ++r) {
                             const uint32_t cd = (__shfl_sync(FULL, cw[r], 2 * s + (lane >> 4)) >> (2 * (lane & 15))) & 3u;
+                            cds[r] = cd;
                             rsv |= cd == 3u;
                             cn += (cd == 1u) - (cd == 2u);
                         }
@@ -259,8 +270,15 @@ __global__ void __launch_bounds__(256, 2) k_fused_ldg(FusedArgs a, KeyTab kt, De
                         if (!a_off) {
                             float wn;
                             if constexpr (APPLY == APPLY_Q) {
-                                wn = __fsub_rn(a.W[e], s_upd[cn + NR]);
-                                isq += cn * cn;
+                                if (a.exact) {
+                                    wn = __fsub_rn(a.W[e], s_upd[cn + NR]);
+                                    isq += cn * cn;
+                                } else {  // sequential ascending-rank fp64 sum, as K2's generic path
+                                    bool r2 = false;
+                                    const double mean = apply_mean_general(cds, NR, a.alpha, a.inv_n_or_zero, r2);
+                                    wn = __fsub_rn(a.W[e], __double2float_rn(__dmul_rn(a.eta_g_d, mean)));
+                                    if (a.gnorm != nullptr) gsq = __fma_rn(mean, mean, gsq);
+                                }
                                 if (rsv) bad_sym = static_cast<uint64_t>(e) < bad_sym ? static_cast<uint64_t>(e) : bad_sym;
                             } else if constexpr (APPLY == APPLY_F) {
                                 const float sv1 = a.gsum[e];

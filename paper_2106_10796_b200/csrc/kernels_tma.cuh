@@ -107,8 +107,10 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
     using SM = QuantSmem<G, WARPS, S>;
     extern __shared__ __align__(128) unsigned char smem[];
     pdl_enter(nullptr, nullptr);
-    p2p_wait(x);  // fused exchange: peers have released the slot we are about to fill
-    const bool aborted = err != nullptr && *reinterpret_cast<volatile uint64_t*>(err) != NO_ERR;
+    const bool peer_failed = p2p_wait(x);  // fused exchange: peers have released the slot we are about to fill
+    // sticky abort: only errors of EARLIER rounds (smaller tag) stop the kernel, so one CTA's
+    // finding never suppresses another CTA's scan of this round (first index stays exact)
+    const bool aborted = peer_failed || (err != nullptr && *reinterpret_cast<volatile uint64_t*>(err) < tag);
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     unsigned char* ring = smem + warp * SM::WARP;

@@ -261,6 +261,8 @@ class CDSGDWorker:
             )
         if rc == _lib.ERR_CORRUPT:
             raise CorruptPayloadError(_lib.last_error())
+        if rc == _lib.ERR_PEER:
+            raise _lib.PeerFailedError(_lib.last_error(), rc)
         raise _lib.LibraryError(_lib.last_error(), rc)
 
     def join(self, stream=None) -> None:

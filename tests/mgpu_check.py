@@ -77,6 +77,34 @@ def run_case(case, exchange, comm, rank, world, dev):
     wk.close()
 
 
+def run_failure_case(exchange, comm, rank, world, dev):
+    """Rank world-1 hits a non-finite gradient at round 2 (a compressed round): it raises
+    CodecNumericError(round 2) with its residual rolled back, every other rank raises
+    PeerFailedError (its flags arrived poisoned) instead of applying the failing rank's
+    codes — and nobody hangs or times out."""
+    from paper_2106_10796_b200.codec import CodecNumericError
+
+    sizes = [4096, 100]
+    layout = Layout.from_lengths(sizes)
+    n = layout.total
+    hp = HyperParams(algo="cdsgd", workers=world, eta_global=0.1, eta_local=0.4, k=4, alpha=0.5, warmup_n=0)
+    wk = CDSGDWorker(layout, hp, O.synthetic_weights(9, n), rank=rank, comm=comm, exchange=exchange)
+    bad = rank == world - 1
+    for t in range(7):
+        g = torch.from_numpy(O.synthetic_grad(9, t, rank, n)).to(dev)
+        if bad and t == 2:
+            g[4096 + 17] = float("nan")
+        wk.step(g)
+    try:
+        wk.check()
+        raise AssertionError(f"rank {rank}: no error reported")
+    except CodecNumericError as exc:
+        assert bad and (exc.round, exc.key, exc.index) == (2, 1, 17), (rank, exc.round, exc.key, exc.index)
+    except _lib.PeerFailedError:
+        assert not bad, f"rank {rank}: PeerFailedError on the failing rank"
+    wk.close()
+
+
 def main():
     rank, world, local = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"]), int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
@@ -88,6 +116,8 @@ def main():
     for exchange in exchanges:
         for case in CASES:
             run_case(case, exchange, comm, rank, world, dev)
+        if exchange in ("p2p", "p2p-exact"):
+            run_failure_case(exchange, comm, rank, world, dev)
     comm.close()
     dist.barrier(device_ids=[local])
     if rank == 0:
