@@ -52,6 +52,8 @@ def parse():
                          "nccl: ncclAllGather + ncclAllReduce")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="budget of the cpu_baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-python-ref", action="store_true", help="skip timing the unmodified Python reference")
+    ap.add_argument("--no-self-check", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-secondary", action="store_true", help="skip the ResNet-20 (configs[1]) line at N=1")
     return ap.parse_args()
@@ -144,64 +146,72 @@ def ncu_traffic(workload: str, kernel: str):
 # ----------------------------------------------------------------------------- CPU legs
 
 
-def cpu_sample_layout(layout, budget_elems):
-    """First keys of the layout totalling ~budget_elems (a bounded sample of the workload)."""
-    from paper_2106_10796_b200.layout import Layout
+def python_reference(layout, args, n_workers, budget_s=40.0):
+    """The UNMODIFIED reference (baseline/_ref, pure Python/NumPy, 1 core) on the same host:
+    its lock-step step loop on the full workload layout for a few rounds, on BASELINE
+    config (i) (1M elements x 2 workers, k=4), and its own `cli bench-codec` harness at
+    16,384 and 1M elements."""
+    from oracle import ref_python
 
-    spans, tot = [], 0
-    for s in layout.spans:
-        if tot >= budget_elems and spans:
-            break
-        spans.append((s.name, s.length))
-        tot += s.length
-    return Layout(spans)
+    if not ref_python.available():
+        return {"unavailable": "reference not installed in baseline/_ref (see DESIGN.md §8)"}
+    out = {"impl": "cdsgd 0.1.0 unmodified (pip-installed into baseline/_ref), single thread"}
+    t0 = time.perf_counter()
+    out["config_i"] = ref_python.run_lockstep([1 << 20], 2, 12, 4, args.alpha)
+    per_round = 0.8 * n_workers * layout.total / 1e6 * 0.06  # ~60 ms per 1M elements per worker (survey host)
+    rounds = int(max(3, min(8, budget_s / max(per_round, 1e-3))))
+    out["workload"] = ref_python.run_lockstep(layout.lengths, n_workers, rounds, args.k, args.alpha)
+    out["workload"]["layout"] = args.workload
+    out["bench_codec_16k"] = ref_python.run_bench_codec(16384, 50)
+    out["bench_codec_1m"] = ref_python.run_bench_codec(1 << 20, 10)
+    out["seconds"] = time.perf_counter() - t0
+    return out
 
 
 def cpu_baseline(layout, args, n_workers):
-    from oracle import cpu_port
+    """C port of the reference round on ALL host threads over the FULL workload layout (no
+    sample), whole k-periods, ~args.cpu_seconds; beside it the unmodified Python reference."""
+    from oracle import cpu_port, ref_python
 
-    sample = cpu_sample_layout(layout, 4_000_000)
-    # calibrate on one period (after an untimed warm-up round), then size the timed run to the
-    # budget in whole k-periods
-    tk, kind, cores, impl = cpu_port.time_rounds(sample.lengths, n_workers, args.k, args.alpha, args.k)
+    tk, kind, cores, impl = cpu_port.time_rounds(layout.lengths, n_workers, args.k, args.alpha, args.k)
     rounds = max(args.k, int(args.cpu_seconds / max(tk / args.k, 1e-6)) // args.k * args.k)
-    secs, kind, cores, impl = cpu_port.time_rounds(sample.lengths, n_workers, args.k, args.alpha, rounds)
-    value = n_workers * sample.total * rounds / secs / 1e9
+    secs, kind, cores, impl = cpu_port.time_rounds(layout.lengths, n_workers, args.k, args.alpha, rounds)
+    value = n_workers * layout.total * rounds / secs / 1e9
     return {"value": value, "unit": UNIT, "cores": cores, "kind": kind,
-            "sample": f"{rounds} lock-step rounds x {n_workers} worker(s) on the first {len(sample)} keys "
-                      f"({sample.total:,} elements) of the {args.workload} layout, k={args.k}; {impl}; "
-                      f"{secs:.1f} s"}
+            "sample": f"{rounds} lock-step rounds x {n_workers} worker(s) on the FULL {args.workload} layout "
+                      f"({len(layout)} keys, {layout.total:,} elements), k={args.k}; {impl}; {secs:.1f} s "
+                      f"(a stronger-than-reference baseline: the reference itself is single-threaded Python, "
+                      f"see python_reference)",
+            "host": ref_python.host_info(),
+            "python_reference": None if args.no_python_ref else python_reference(layout, args, n_workers)}
 
 
 def run_reference(args):
-    """--impl reference: the reference algorithm's CPU port on the host cores, rank 0 only."""
+    """--impl reference: the reference algorithm on the host cores, rank 0 only. value = the C
+    restatement (bit-identical to the reference round) on all host threads over the FULL
+    layout; python_reference = the unmodified reference itself (1 thread) beside it."""
     rank, world, _ = env_rank()
     if rank != 0:
         return 0
-    from oracle import cpu_port
+    from oracle import cpu_port, ref_python
     from paper_2106_10796_b200.layout import by_name
 
     layout = by_name(args.workload)
     n_workers = max(args.gpus, world)
-    sample = cpu_sample_layout(layout, 2_000_000)
-    tk, kind, cores, impl = cpu_port.time_rounds(sample.lengths, n_workers, args.k, args.alpha, args.k)
-    t1 = tk / args.k
-    # each step is a bounded sample sized so warmup+steps finish in ~2-3 minutes
-    per_step_budget = 150.0 / max(1, args.steps + args.warmup)
-    scale = max(0.05, min(1.0, per_step_budget / max(t1, 1e-6)))
-    sample = cpu_sample_layout(layout, int(sample.total * scale))
-    secs, kind, cores, impl = cpu_port.time_rounds(sample.lengths, n_workers, args.k, args.alpha, args.steps,
+    secs, kind, cores, impl = cpu_port.time_rounds(layout.lengths, n_workers, args.k, args.alpha, args.steps,
                                                    warm=max(1, args.warmup))
-    value = n_workers * sample.total * args.steps / secs / 1e9
-    desc = (f"{args.steps} lock-step rounds x {n_workers} simulated workers on the first {len(sample)} keys "
-            f"({sample.total:,} elements) of the {args.workload} layout; {impl}")
+    value = n_workers * layout.total * args.steps / secs / 1e9
+    desc = (f"{args.steps} lock-step rounds x {n_workers} simulated workers on the FULL {args.workload} layout "
+            f"({len(layout)} keys, {layout.total:,} elements), after {max(1, args.warmup)} untimed; {impl}")
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * secs / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
         "config": {"workload": workload_desc(layout, args.workload), "k": args.k, "alpha": args.alpha,
                    "algo": "cdsgd", "parallelism": f"dp{n_workers} (simulated, host)"},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind, "sample": desc},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind, "sample": desc,
+                         "host": ref_python.host_info()},
+        "python_reference": None if args.no_python_ref else python_reference(layout, args, n_workers),
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -287,6 +297,136 @@ def small_layout_rate(args, dev, name="resnet20", steps=400, warmup=20):
 
 
 
+def small_layout_cold(args, dev, name="resnet20", n_sets=48, rounds=8):
+    """The same small layout with COLD L2: n_sets independent workers (each with its own W,
+    residuals, codes and gradients; > 126 MB L2 in total) stepped round-robin, so every
+    step's inputs were evicted by the other sets' steps (SURVEY §8d config ii)."""
+    import torch
+
+    from paper_2106_10796_b200.engine import HyperParams
+    from paper_2106_10796_b200.layout import by_name
+    from paper_2106_10796_b200.worker import CDSGDWorker
+
+    layout = by_name(name)
+    n = layout.total
+    hp = HyperParams(algo="cdsgd", workers=1, eta_global=0.1, eta_local=0.4, k=args.k, alpha=args.alpha, warmup_n=0)
+    gen = torch.Generator(device=dev).manual_seed(11)
+    sets = [(CDSGDWorker(layout, hp, torch.zeros(n, device=dev), gnorm_ring=8),
+             [0.3 * torch.randn(n, device=dev, generator=gen) for _ in range(2)]) for _ in range(n_sets)]
+    per_set = n * (4 * 2 + 8 * 2 + 4 * 2 + 4 * 2) + 2 * layout.n_words * 4  # g x2, r x2, W, loc, codes
+    for r in range(args.k):
+        for wk, pool in sets:
+            wk.step(pool[r % 2])
+    torch.cuda.synchronize(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for r in range(rounds):
+        for wk, pool in sets:
+            wk.step(pool[r % 2])
+    e1.record()
+    e1.synchronize()
+    ms = e0.elapsed_time(e1)
+    for wk, _ in sets:
+        wk.check()
+        wk.close()
+    steps = rounds * n_sets
+    return {"value": n * steps / (ms / 1e3) / 1e9, "unit": UNIT, "ms_per_step": ms / steps, "steps": steps,
+            "how": f"{n_sets} independent workers stepped round-robin ({n_sets * per_set / 2**20:.0f} MiB of "
+                   f"state+inputs > 126 MB L2): each step starts from cold L2"}
+
+
+def allreduce_standalone(comm, n, dev, reps=20):
+    """Bus bandwidth of the correction all-reduce ALONE (nothing else on the GPU): the same
+    ncclAllReduce(fp32 sum) of n elements on the engine's communicator (nccl-tests bus bytes
+    2(N-1)/N * 4n)."""
+    import torch
+
+    a = torch.randn(n, device=dev)
+    b = torch.empty_like(a)
+    for _ in range(3):
+        comm.allreduce_sum(a, b)
+    torch.cuda.synchronize(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        comm.allreduce_sum(a, b)
+    e1.record()
+    e1.synchronize()
+    us = 1e3 * e0.elapsed_time(e1) / reps
+    bus = 2 * (comm.world - 1) / comm.world * 4 * n
+    return {"us": us, "bus_gbs": bus / us / 1e3, "bus_frac_of_900": bus / us / 1e3 / 900.0,
+            "bus_frac_of_measured_770": bus / us / 1e3 / 770.0}
+
+
+def self_check(wk, layout, pools, seq, w0, world, rank, dev, args, keys=(0, None, -1)):
+    """Parity of the run just measured, computed after the timed regions:
+    * W replicas: rank 0 gathers every rank's W and compares them bitwise (the replicated
+      server must stay identical, DESIGN §6);
+    * replay: the C restatement of the reference round (oracle/cdsgd_oracle.c, pinned to the
+      reference's golden traces) re-runs EVERY round of this process (warm-up, timed,
+      profiled and e2e steps: the recorded gradient-pool sequence) for a few keys with all
+      ranks' gradients, then compares each rank's fp64 residual bitwise and W / loc within
+      rtol 1e-5, atol 1e-6 (reference: engine.py:614-663)."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    t0 = time.perf_counter()
+    wk.flush()
+    torch.cuda.synchronize(dev)
+    W = wk.weights.contiguous()
+    if world > 1:
+        allW = torch.empty((world, W.numel()), dtype=W.dtype, device=dev)
+        dist.all_gather_into_tensor(allW, W)
+        same = all(torch.equal(allW[r], allW[0]) for r in range(world))
+    else:
+        same = True
+    spans = layout.spans
+    idx = sorted({k % len(spans) if k is not None else len(spans) // 2 for k in keys})
+    eoff = [0]
+    for sp in spans:
+        eoff.append(eoff[-1] + sp.length)
+    sl = [(eoff[k], eoff[k + 1]) for k in idx]
+    cat = lambda t: torch.cat([t[a:b] for a, b in sl])  # noqa: E731
+    mine = {"g0": cat(pools[0]), "g1": cat(pools[1]), "res": cat(wk.residual), "loc": cat(wk.compute_weights()),
+            "W": cat(W)}
+    if world > 1:
+        got = {}
+        for k, v in mine.items():
+            buf = torch.empty((world, v.numel()), dtype=v.dtype, device=dev)
+            dist.all_gather_into_tensor(buf, v.contiguous())
+            got[k] = buf.cpu().numpy()
+    else:
+        got = {k: v.cpu().numpy()[None] for k, v in mine.items()}
+    out = {"replicas_bitwise_equal": bool(same)}
+    if rank == 0:
+        from oracle import cpu_port
+
+        if cpu_port.load() is None:
+            out["replay"] = "C port not built"
+        else:
+            sizes = [b - a for a, b in sl]
+            w0s = np.concatenate([w0[a:b] for a, b in sl]).astype(np.float64)
+            port = cpu_port.CPortEngine(w0s, sizes, world, k=args.k, alpha=args.alpha, eta_g=0.1, eta_l=0.4)
+            for p in seq:
+                port.step(got["g0"] if p == 0 else got["g1"])
+            res_ok = all(np.array_equal(got["res"][r].view(np.uint64), port.res[r].view(np.uint64))
+                         for r in range(world))
+            dW = np.abs(got["W"][0].astype(np.float64) - port.W)
+            dl = max(float(np.abs(got["loc"][r].astype(np.float64) - port.loc[r]).max()) for r in range(world))
+            w_ok = bool(np.all(dW <= 1e-6 + 1e-5 * np.abs(port.W)))
+            l_ok = all(bool(np.all(np.abs(got["loc"][r].astype(np.float64) - port.loc[r])
+                                   <= 1e-6 + 1e-5 * np.abs(port.loc[r]))) for r in range(world))
+            out.update({"keys_replayed": [spans[k].name for k in idx], "elements_replayed": int(sum(sizes)),
+                        "rounds_replayed": len(seq), "residual_bitwise": bool(res_ok), "W_within_tol": w_ok,
+                        "loc_within_tol": l_ok, "W_max_abs_err": float(dW.max()), "loc_max_abs_err": dl,
+                        "tolerance": "rtol 1e-5, atol 1e-6"})
+        out["ok"] = bool(same and out.get("residual_bitwise", True) and out.get("W_within_tol", True)
+                         and out.get("loc_within_tol", True))
+        out["seconds"] = time.perf_counter() - t0
+    return out
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -331,8 +471,10 @@ def run_ours(args):
 
     # ---------------- device-resident timed region
     W, K = max(args.warmup, 3), args.steps
+    seq = []  # gradient-pool index of every round this worker runs (self-check replay)
     for i in range(W):
         wk.step(pool[i % 2])
+        seq.append(i % 2)
     wk.join()
     wk.check()
     barrier()
@@ -345,6 +487,7 @@ def run_ours(args):
         wk.step(pool[(W + i) % 2])
     wk.join()
     ev1.record(stream)
+    seq += [(W + i) % 2 for i in range(K)]
     ev1.synchronize()
     launches = _lib.launch_count() - l0
     clk = clocks.stop()
@@ -361,6 +504,7 @@ def run_ours(args):
     for i in range(K):
         wk.step(pool[(W + K + i) % 2])
     wk.join()
+    seq += [(W + K + i) % 2 for i in range(K)]
     pe1.record(stream)
     pe1.synchronize()
     prof = wk.profile_end()
@@ -419,6 +563,19 @@ def run_ours(args):
             exch.update({"nccl_calls": prof["exchange"]["n"], "nccl_total_ms": prof["exchange"]["ms"],
                          "nccl_bus_gbs": bus_bytes / (prof["exchange"]["ms"] / 1e3) / 1e9, "nvlink_peak_gbs": 900.0})
             exch["nccl_bus_frac"] = exch["nccl_bus_gbs"] / 900.0
+        if not nccl_codes:
+            # the code all-gather runs inside the fused / quantizing kernels: (N-1)*P bytes leave
+            # each rank per compressed round over the kernel's duration
+            kq = [kk for kk in ("fused", "quantize") if prof[kk]["n"]]
+            qms = sum(prof[kk]["ms"] for kk in kq)
+            qn = sum(prof[kk]["n"] for kk in kq)
+            if qn:
+                exch.update({"code_kernel_avg_us": 1e3 * qms / qn,
+                             "code_bus_gbs_in_kernel": (world - 1) * P / (qms / qn / 1e3) / 1e9})
+        if comm is not None:
+            exch["allreduce_standalone"] = allreduce_standalone(comm, n, dev)
+            exch["allreduce_standalone"]["what"] = ("ncclAllReduce(fp32 sum) of the full 4n-byte correction "
+                                                    "alone on the engine's communicator, 20 reps")
         if prof["exchange_ce"]["n"]:
             ce_bytes = n_full * cef * ar_bus
             exch.update({"ce_calls": prof["exchange_ce"]["n"], "ce_total_ms": prof["exchange_ce"]["ms"],
@@ -468,12 +625,18 @@ def run_ours(args):
                "d2h_bytes_per_step": 8, "ms_per_step": ems / K,
                "path": "CDSGDWorker.step (public API -> C ABI) with the gradient copied from pinned host memory "
                        "on a copy stream each step and the round's grad-norm read back to pinned host"}
+        seq += [(i % 3) % 2 for i in range(K)]  # host[s] holds pool[s % 2]
+
+    check = None
+    if not args.no_self_check:
+        check = self_check(wk, layout, pool, seq, w0.cpu().numpy(), world, rank, dev, args)
 
     # configs[1] of BASELINE.json: the ResNet-20/CIFAR-10-sized gradient on one B200
     # (quantize + apply kernels only) — measured beside the headline when N=1
     secondary = None
     if world == 1 and args.workload == "resnet50" and not args.no_secondary:
         secondary = {"resnet20": small_layout_rate(args, dev)}
+        secondary["resnet20"]["cold_l2"] = small_layout_cold(args, dev)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -492,7 +655,7 @@ def run_ours(args):
                              f"HBM traffic per step per rank vs 126 MB L2",
                        "parallelism": f"dp{world}"},
             "roofline": roof, "kernels": kernels, "waits": waits, "exchange": exch, "cpu_baseline": cpu, "e2e": e2e,
-            "secondary": secondary,
+            "secondary": secondary, "self_check": check,
             "gpu_launches": launches, "clocks": clk,
         }
         print(json.dumps(line), flush=True)

@@ -157,9 +157,17 @@ bool prepare_tma(K kernel, int smem_bytes) {
     if (nseen < 64) seen[nseen++] = Key{reinterpret_cast<const void*>(kernel), d};
     return true;
 }
+// SMs the engine leaves free for the exchange while a correction all-reduce is in flight
+// (0 = none): the TMA kernels (1 CTA per SM) and the wide K2 are capped at SMs - reserve.
+thread_local int tl_reserve_sms = 0;
+struct ReserveScope {
+    int prev;
+    explicit ReserveScope(int r) : prev(tl_reserve_sms) { tl_reserve_sms = r; }
+    ~ReserveScope() { tl_reserve_sms = prev; }
+};
 inline int tma_grid(int64_t ntiles, int warps) {
     const int64_t want = (ntiles + warps - 1) / warps;
-    const int64_t cap = dev_info().sms;
+    const int64_t cap = std::max(1, dev_info().sms - tl_reserve_sms);
     return static_cast<int>(want < cap ? (want > 0 ? want : 1) : cap);
 }
 // Tuning knobs for development sweeps: CDSGD_TMA_CFG (K1) / CDSGD_TMA_CFG2 (K2, K3) = <warps>x<stages>.
@@ -474,6 +482,17 @@ int launch_apply_quant(const cdsgd_layout* L, float* W, const uint32_t* gathered
     }
     a.exact = exact;
     const KeyTab kt = L->tab();
+    if (tl_reserve_sms > 0 && nr > 1 && nr <= 8 && a.sched != nullptr) {
+        // beside a correction all-reduce: one 512-thread CTA per SM on SMs - reserve (the
+        // dynamic tile scheduler balances the work over however many CTAs run)
+        const int grid = std::max(1, dev_info().sms - tl_reserve_sms);
+#define AQW(R) \
+    case R: launch_pdl(k_apply_quant<R, 1>, grid, 2 * THREADS, 0, st, a, kt, tab); break
+        switch (nr) { AQW(2); AQW(3); AQW(4); AQW(5); AQW(6); AQW(7); AQW(8); }
+#undef AQW
+        LAUNCH_CHECK();
+        return CDSGD_OK;
+    }
 #define AQ(R)                                                                                   \
     case R:                                                                                     \
         launch_pdl(k_apply_quant<R>, tile_grid(k_apply_quant<R>, kt.ntiles), THREADS, 0, st, a, kt, tab); \
@@ -715,6 +734,8 @@ struct cdsgd_engine {
     bool fuse = false;                 // apply(t-1) + quantize(t) in one kernel (N=1 or P2P)
     bool pcorr = false;                // P2P mode: correction rounds by the exact sharded NVLink reduce
     bool plain_after_ar = false;       // plain (non-PDL) launch of the apply beside a correction all-reduce
+    int reserve_sms = 0;               // SMs left free for the all-reduce's CTAs (CDSGD_RESERVE_SMS)
+    int64_t ar_round = -1;             // correction round whose all-reduce is in flight on the exchange streams
     bool diag_local_codes = false;     // timing diagnostic: store codes only locally
     bool diag_no_wait = false;         // timing diagnostic: skip the code-exchange flag waits
     int sc_fence = 0;                  // CDSGD_SC_FENCE=1: fence.sc.sys publish (A/B knob)
@@ -1091,6 +1112,8 @@ extern "C" int cdsgd_engine_create(const cdsgd_engine_desc* d, const cdsgd_layou
         E->fuse = d->nranks == 1 && !(nf != nullptr && nf[0] == '1');
         // A/B knob: plain launch of the apply beside a correction all-reduce (measured no gain at
         // N=2: 296 vs 301 Gelem/s — the apply's CTAs fill every SM either way)
+        const char* rs = getenv("CDSGD_RESERVE_SMS");
+        E->reserve_sms = rs != nullptr ? std::max(0, atoi(rs)) : 0;
         const char* pa = getenv("CDSGD_PLAIN_AFTER_AR");
         E->plain_after_ar = pa != nullptr && pa[0] == '1';
         const char* ns = getenv("CDSGD_STATIC_SCHED");
@@ -1437,8 +1460,10 @@ extern "C" int cdsgd_engine_step(cdsgd_engine* E, const float* g, void* stream) 
         E->t = t + 1;
         return CDSGD_OK;
     }
-    // 1. this round's contribution (K1 on compressed rounds)
+    // 1. this round's contribution (K1 on compressed rounds); right after a correction round
+    // its all-reduce is still in flight (ReserveScope: leave SMs to its CTAs)
     E->rlog.push_back(static_cast<int8_t>(E->rcur));
+    const ReserveScope reserve1(E->ar_round >= 0 && E->ar_round == t - 1 ? E->reserve_sms : 0);
     if (comp) {
         const uint64_t tag = static_cast<uint64_t>(t - E->err_base) << CDSGD_INDEX_BITS;
         const long pi = prof_start(E, 0, C);
@@ -1515,6 +1540,10 @@ extern "C" int cdsgd_engine_step(cdsgd_engine* E, const float* g, void* stream) 
     }
     // 3. apply
     const PlainLaunchScope plain(E->xused[t & 1] && !comp && E->plain_after_ar);
+    // the all-reduce of correction round t is in flight from here until K3(t) waits for it:
+    // the apply below (K2(t-1)) and the next round's quantize run beside it
+    if (E->xused[t & 1] && !comp) E->ar_round = t;
+    const ReserveScope reserve3(E->xused[t & 1] && !comp ? E->reserve_sms : 0);
     const bool sync_path = !E->uses_local || t < E->n_warmup - 1;
     if (sync_path) {
         if (E->pending) return fail(CDSGD_ERR_STATE, "internal: pending round on the synchronous path");

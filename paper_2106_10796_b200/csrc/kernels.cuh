@@ -554,13 +554,17 @@ __device__ __forceinline__ void apply_vec_tile(const ApplyQArgs& a, const float*
     }
 }
 
-template <int NR>  // NR > 0: compile-time rank count; NR == 0: runtime (generic)
+// NR > 0: compile-time rank count; NR == 0: runtime (generic).
 // 3 CTAs per SM at N=1 (80 registers, a 24-byte spill): 88 -> 82 us at ResNet-50 size, the
 // extra warps keep more loads in flight; more ranks spill more, so they keep 2.
+// WIDE = 1: one 512-thread CTA per SM (the same 16 warps and register budget as 2 x 256), so
+// a grid of (SMs - R) CTAs leaves R whole SMs free — launched beside a correction all-reduce,
+// whose NCCL CTAs (104 KB smem, 52K registers each) cannot share an SM with this kernel.
 #ifndef CDSGD_K2_MINB
 #define CDSGD_K2_MINB (NR == 1 ? 3 : 2)
 #endif
-__global__ void __launch_bounds__(256, CDSGD_K2_MINB) k_apply_quant(ApplyQArgs a, KeyTab kt, DecodeTab tab) {
+template <int NR, int WIDE = 0>
+__global__ void __launch_bounds__(WIDE ? 512 : 256, WIDE ? 1 : CDSGD_K2_MINB) k_apply_quant(ApplyQArgs a, KeyTab kt, DecodeTab tab) {
     pdl_enter(a.gclear[0], a.gclear[1]);
     const bool peer_failed = p2p_wait2(a.x, a.xs);
     const bool skip = peer_failed || (a.err != nullptr && *reinterpret_cast<volatile uint64_t*>(a.err) < a.skip_below);
