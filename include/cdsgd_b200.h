@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define CDSGD_ABI_VERSION 1
+#define CDSGD_ABI_VERSION 2
 
 #define CDSGD_OK 0
 #define CDSGD_ERR_ARG -1     /* bad argument: maps to CodecError / LayoutError / ConfigError */
@@ -122,18 +122,19 @@ int cdsgd_local_update(const void* base, int32_t base_dtype, const void* grad, i
 
 /* ------------------------------------------------------------------ fused apply (K2/K3)
  * K2 — compressed round: ServerNode._handle_push's decode + ascending-worker sum
- * + /N + W -= eta_g*mean (engine.py:249-255, 509-511) on a replicated fp32 W,
+ * + /N + W -= eta_g*mean (engine.py:249-255, 509-511) on a replicated W of w_dtype
+ * (CDSGD_F64: the reference's own fp64 operations; CDSGD_F32: one fp32 rounding per round),
  * fused with the next local update loc = W' - eta_l*g_next (engine.py:385-392,
  * Eq. 11). `gathered` holds nranks payload buffers, rank r at r*rank_stride_words.
  * g_next / loc_out may be NULL (no local update). gnorm_sq (nullable) receives
  * += sum(mean^2) (engine.py:521). Skips all work if *err < skip_below. */
-int cdsgd_apply_quant(const cdsgd_layout* layout, float* weights, const uint32_t* gathered,
+int cdsgd_apply_quant(const cdsgd_layout* layout, void* weights, int32_t w_dtype, const uint32_t* gathered,
                       int32_t nranks, int64_t rank_stride_words, double alpha, double eta_g,
                       const float* g_next, float* loc_out, double eta_l, uint64_t* err,
                       uint64_t skip_below, double* gnorm_sq, void* stream);
 /* K3 — correction round (engine.py:252 full branch + 511): W -= eta_g * gsum/nranks,
  * then loc = W' - eta_l*g_next. gsum is the (NCCL) fp32 sum over ranks. */
-int cdsgd_apply_full(float* weights, const float* gsum, int32_t nranks, int64_t n, double eta_g,
+int cdsgd_apply_full(void* weights, int32_t w_dtype, const float* gsum, int32_t nranks, int64_t n, double eta_g,
                      const float* g_next, float* loc_out, double eta_l, const uint64_t* err,
                      uint64_t skip_below, double* gnorm_sq, void* stream);
 
@@ -147,8 +148,8 @@ int cdsgd_apply_full(float* weights, const float* gsum, int32_t nranks, int64_t 
  * when every j*alpha is representable, else the sequential fp64 sum). gnorm_sq: += the
  * round t-1 mean's sum of squares (nullable). */
 int cdsgd_fused_round(const cdsgd_layout* layout, const float* grad, const double* r_in, double* r_out,
-                      uint32_t* words, double alpha, uint64_t* err, uint64_t err_tag, float* weights,
-                      float* loc, const uint32_t* gathered, int32_t nranks, int64_t rank_stride_words,
+                      uint32_t* words, double alpha, uint64_t* err, uint64_t err_tag, void* weights,
+                      int32_t w_dtype, float* loc, const uint32_t* gathered, int32_t nranks, int64_t rank_stride_words,
                       double eta_g, double eta_l, uint64_t skip_below, double* gnorm_sq, void* stream);
 
 /* ------------------------------------------------------------------ exchange (NCCL)
@@ -193,8 +194,10 @@ typedef struct {
     int32_t force_compress; /* engine.py:300, 351-352 */
     int32_t bypass_local;   /* engine.py:301, 310 */
     int32_t gnorm_ring;     /* entries in gnorm_sq (0 = no grad-norm metric) */
+    int32_t weights_dtype;  /* CDSGD_F64: exact (the reference's fp64 W, bitwise on compressed rounds);
+                               CDSGD_F32: fast (W rounded to fp32 every round) */
     double alpha, eta_global, eta_local;
-    float* weights;          /* [n] fp32, replicated global weights W */
+    void* weights;           /* [n] fp64 or fp32 (weights_dtype), replicated global weights W */
     float* loc;              /* [n] fp32, local (compute) weights */
     double* residual[2];     /* [n] fp64 each, ping-pong error-feedback residual */
     uint32_t* gathered[2];   /* [nranks * words] each */

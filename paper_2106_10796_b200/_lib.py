@@ -21,6 +21,8 @@ INDEX_BITS = 40
 F32, F64 = 0, 1
 ALGO = {"ssgd": 0, "lusgd": 1, "bitsgd": 2, "cdsgd": 3}
 UNIQUE_ID_BYTES = 128
+ABI_VERSION = 2
+WEIGHTS = {"f64": 1, "f32": 0}  # CDSGD_F64 (exact, default) / CDSGD_F32 (fast)
 
 vp = C.c_void_p
 i32 = C.c_int32
@@ -32,7 +34,7 @@ f64 = C.c_double
 class EngineDesc(C.Structure):
     _fields_ = [
         ("algo", i32), ("nranks", i32), ("rank", i32), ("k", i32), ("warmup_n", i32),
-        ("force_compress", i32), ("bypass_local", i32), ("gnorm_ring", i32),
+        ("force_compress", i32), ("bypass_local", i32), ("gnorm_ring", i32), ("weights_dtype", i32),
         ("alpha", f64), ("eta_global", f64), ("eta_local", f64),
         ("weights", vp), ("loc", vp), ("residual", vp * 2), ("gathered", vp * 2), ("gsum", vp * 2),
         ("err", vp), ("gnorm_sq", vp),
@@ -64,9 +66,9 @@ _SIGS = {
     "cdsgd_unpack_symbols": (C.c_int, [vp, i64, vp, vp]),
     "cdsgd_global_update": (C.c_int, [vp, i32, vp, i32, i64, f64, vp]),
     "cdsgd_local_update": (C.c_int, [vp, i32, vp, i32, vp, i32, i64, f64, vp]),
-    "cdsgd_apply_quant": (C.c_int, [vp, vp, vp, i32, i64, f64, f64, vp, vp, f64, vp, u64, vp, vp]),
-    "cdsgd_apply_full": (C.c_int, [vp, vp, i32, i64, f64, vp, vp, f64, vp, u64, vp, vp]),
-    "cdsgd_fused_round": (C.c_int, [vp, vp, vp, vp, vp, f64, vp, u64, vp, vp, vp, i32, i64, f64, f64, u64, vp, vp]),
+    "cdsgd_apply_quant": (C.c_int, [vp, vp, i32, vp, i32, i64, f64, f64, vp, vp, f64, vp, u64, vp, vp]),
+    "cdsgd_apply_full": (C.c_int, [vp, i32, vp, i32, i64, f64, vp, vp, f64, vp, u64, vp, vp]),
+    "cdsgd_fused_round": (C.c_int, [vp, vp, vp, vp, vp, f64, vp, u64, vp, i32, vp, vp, i32, i64, f64, f64, u64, vp, vp]),
     "cdsgd_comm_unique_id": (C.c_int, [vp]),
     "cdsgd_comm_init": (C.c_int, [vp, i32, i32, C.POINTER(vp)]),
     "cdsgd_comm_destroy": (C.c_int, [vp]),
@@ -121,7 +123,7 @@ def load(path: str = LIB_PATH):
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args
-    if lib.cdsgd_abi_version() != 1:
+    if lib.cdsgd_abi_version() != ABI_VERSION:
         raise LibraryError("libcdsgd_b200.so ABI version mismatch")
     _lib = lib
     return lib

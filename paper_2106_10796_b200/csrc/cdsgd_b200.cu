@@ -185,15 +185,17 @@ int tma_cfg2() {  // K3
     static const int v = read_cfg("CDSGD_TMA_CFG2", 84);
     return v;
 }
-template <int WP, int ST>
+template <int WP, int ST, typename TW = float>
 int launch_af_tma(const ApplyFArgs& a, cudaStream_t st) {
-    using SM = ApplyFSmem<WP, ST>;
+    using SM = ApplyFSmem<WP, ST, TW>;
     static_assert(SM::BYTES <= 227 * 1024, "smem");
-    if (!prepare_tma(k_apply_full_tma<WP, ST>, SM::BYTES)) return fail(CDSGD_ERR_CUDA, "smem attribute");
-    launch_pdl(k_apply_full_tma<WP, ST>, tma_grid((a.n + TILE_ELEMS - 1) / TILE_ELEMS, WP), WP * 32, SM::BYTES, st, a);
+    if (!prepare_tma(k_apply_full_tma<WP, ST, TW>, SM::BYTES)) return fail(CDSGD_ERR_CUDA, "smem attribute");
+    launch_pdl(k_apply_full_tma<WP, ST, TW>, tma_grid((a.n + TILE_ELEMS - 1) / TILE_ELEMS, WP), WP * 32, SM::BYTES,
+               st, a);
     return CDSGD_OK;
 }
-int launch_af_tma_cfg(const ApplyFArgs& a, cudaStream_t st) {
+int launch_af_tma_cfg(const ApplyFArgs& a, int wdt, cudaStream_t st) {
+    if (wdt == CDSGD_F64) return launch_af_tma<8, 3, double>(a, st);  // 8 KB slots: 3 stages fit
     switch (tma_cfg2()) {
         case 162: return launch_af_tma<16, 2>(a, st);
         case 83: return launch_af_tma<8, 3>(a, st);
@@ -432,13 +434,14 @@ void build_tab(DecodeTab& tab, double alpha, double eta_g, int nr) {
         const double total = static_cast<double>(c) * alpha;          // exact (alpha_exact)
         const double mean = total / static_cast<double>(nr);          // engine.py:255
         tab.mean[c + nr] = mean;
-        tab.upd[c + nr] = static_cast<float>(eta_g * mean);           // engine.py:511 (eta*mean)
+        tab.upd[c + nr] = static_cast<float>(eta_g * mean);           // engine.py:511 (eta*mean), fp32 W
+        tab.upd64[c + nr] = eta_g * mean;                             // the reference's own product, fp64 W
     }
     tab.sq_scale = (alpha / nr) * (alpha / nr);
 }
 inline bool pow2(int n) { return n > 0 && (n & (n - 1)) == 0; }
 
-int launch_apply_quant(const cdsgd_layout* L, float* W, const uint32_t* gathered, int nr, int64_t stride,
+int launch_apply_quant(const cdsgd_layout* L, void* W, int wdt, const uint32_t* gathered, int nr, int64_t stride,
                        double alpha, double eta_g, const float* gnext, float* loc, double eta_l, uint64_t* err,
                        uint64_t skip_below, double* gnorm, const DecodeTab* tab_in, int exact_in,
                        cudaStream_t st, const P2PArgs* x = nullptr, const StageDst* gs = nullptr,
@@ -468,6 +471,7 @@ int launch_apply_quant(const cdsgd_layout* L, float* W, const uint32_t* gathered
     a.xs = xs != nullptr ? *xs : P2PArgs{};
     a.sched = sched;
     a.fold_scale = fold_scale;
+    a.fold = fold_scale != 0.f ? 1 : 0;
     a.gnorm2 = gnorm2;
     a.gclear[0] = gclear != nullptr ? gclear[0] : nullptr;
     a.gclear[1] = gclear != nullptr ? gclear[1] : nullptr;
@@ -486,28 +490,44 @@ int launch_apply_quant(const cdsgd_layout* L, float* W, const uint32_t* gathered
         // beside a correction all-reduce: one 512-thread CTA per SM on SMs - reserve (the
         // dynamic tile scheduler balances the work over however many CTAs run)
         const int grid = std::max(1, dev_info().sms - tl_reserve_sms);
-#define AQW(R) \
-    case R: launch_pdl(k_apply_quant<R, 1>, grid, 2 * THREADS, 0, st, a, kt, tab); break
+#define AQW(R)                                                                                 \
+    case R:                                                                                    \
+        if (wdt == CDSGD_F64) launch_pdl(k_apply_quant<R, 1, double>, grid, 2 * THREADS, 0, st, a, kt, tab); \
+        else launch_pdl(k_apply_quant<R, 1, float>, grid, 2 * THREADS, 0, st, a, kt, tab);         \
+        break
         switch (nr) { AQW(2); AQW(3); AQW(4); AQW(5); AQW(6); AQW(7); AQW(8); }
 #undef AQW
         LAUNCH_CHECK();
         return CDSGD_OK;
     }
-#define AQ(R)                                                                                   \
-    case R:                                                                                     \
-        launch_pdl(k_apply_quant<R>, tile_grid(k_apply_quant<R>, kt.ntiles), THREADS, 0, st, a, kt, tab); \
+#define AQ(R, TW)                                                                                       \
+    case R:                                                                                             \
+        launch_pdl(k_apply_quant<R, 0, TW>, tile_grid(k_apply_quant<R, 0, TW>, kt.ntiles), THREADS, 0, st, a, kt, \
+                   tab);                                                                                \
         break
-    switch (nr) {
-        AQ(1); AQ(2); AQ(3); AQ(4); AQ(5); AQ(6); AQ(7); AQ(8);
-        default:
-            launch_pdl(k_apply_quant<0>, tile_grid(k_apply_quant<0>, kt.ntiles), THREADS, 0, st, a, kt, tab);
+    if (wdt == CDSGD_F64) {
+        switch (nr) {
+            AQ(1, double); AQ(2, double); AQ(3, double); AQ(4, double); AQ(5, double); AQ(6, double); AQ(7, double);
+            AQ(8, double);
+            default:
+                launch_pdl(k_apply_quant<0, 0, double>, tile_grid(k_apply_quant<0, 0, double>, kt.ntiles), THREADS, 0,
+                           st, a, kt, tab);
+        }
+    } else {
+        switch (nr) {
+            AQ(1, float); AQ(2, float); AQ(3, float); AQ(4, float); AQ(5, float); AQ(6, float); AQ(7, float);
+            AQ(8, float);
+            default:
+                launch_pdl(k_apply_quant<0, 0, float>, tile_grid(k_apply_quant<0, 0, float>, kt.ntiles), THREADS, 0, st,
+                           a, kt, tab);
+        }
     }
 #undef AQ
     LAUNCH_CHECK();
     return CDSGD_OK;
 }
 
-int launch_apply_full(float* W, const float* gsum, int nr, int64_t n, double eta_g, const float* gnext,
+int launch_apply_full(void* W, int wdt, const float* gsum, int nr, int64_t n, double eta_g, const float* gnext,
                       float* loc, double eta_l, const uint64_t* err, uint64_t skip_below, double* gnorm,
                       cudaStream_t st, double* const* gclear = nullptr) {
     if (nr < 1) return fail(CDSGD_ERR_ARG, "nranks must be >= 1");
@@ -521,72 +541,81 @@ int launch_apply_full(float* W, const float* gsum, int nr, int64_t n, double eta
     a.scale = static_cast<float>(eta_g / nr);
     a.eta_l = static_cast<float>(eta_l);
     a.inv_n = 1.0 / nr;
+    a.eta_g_d = eta_g;
+    a.eta_l_d = eta_l;
+    a.inv_n_or_zero = pow2(nr) ? 1.0 / nr : 0.0;
+    a.nranks = nr;
     a.n = n;
     a.err = err;
     a.skip_below = skip_below;
     a.gnorm = gnorm;
     a.gclear[0] = gclear != nullptr ? gclear[0] : nullptr;
     a.gclear[1] = gclear != nullptr ? gclear[1] : nullptr;
-    const int rc = launch_af_tma_cfg(a, st);
+    const int rc = launch_af_tma_cfg(a, wdt, st);
     if (rc != CDSGD_OK) return rc;
     LAUNCH_CHECK();
     return CDSGD_OK;
 }
 // Fused apply(t-1) + quantize(t), register-staged (measured faster than a TMA-ring variant).
-template <int NR, int AP>
+template <int NR, int AP, typename TW>
 int launch_fused_cfg(const FusedArgs& a, const KeyTab& kt, const DecodeTab& tab, cudaStream_t st) {
     // fewer than 2 whole-tile tasks per resident warp: split tiles into chunk tasks
-    const int64_t warps = static_cast<int64_t>(resident_blocks(k_fused_ldg<NR, AP, CHUNKS>, THREADS)) * WARPS_PER_BLOCK;
+    const int64_t warps =
+        static_cast<int64_t>(resident_blocks(k_fused_ldg<NR, AP, CHUNKS, TW>, THREADS)) * WARPS_PER_BLOCK;
     if (kt.ntiles < 2 * warps)
-        launch_pdl(k_fused_ldg<NR, AP, 1>, tile_grid(k_fused_ldg<NR, AP, 1>, kt.ntiles * CHUNKS), THREADS, 0, st, a, kt,
-                   tab);
+        launch_pdl(k_fused_ldg<NR, AP, 1, TW>, tile_grid(k_fused_ldg<NR, AP, 1, TW>, kt.ntiles * CHUNKS), THREADS, 0, st,
+                   a, kt, tab);
     else
-        launch_pdl(k_fused_ldg<NR, AP, CHUNKS>, tile_grid(k_fused_ldg<NR, AP, CHUNKS>, kt.ntiles), THREADS, 0, st, a, kt,
-                   tab);
+        launch_pdl(k_fused_ldg<NR, AP, CHUNKS, TW>, tile_grid(k_fused_ldg<NR, AP, CHUNKS, TW>, kt.ntiles), THREADS, 0,
+                   st, a, kt, tab);
     return CDSGD_OK;
 }
-int launch_fused(int nr, int apply, const FusedArgs& a, const KeyTab& kt, const DecodeTab& tab, cudaStream_t st) {
-    int rc;
-    if (apply == APPLY_L) {  // W is final (P2P correction): only loc = W - eta_l*g and quantize
-        rc = launch_fused_cfg<1, APPLY_L>(a, kt, tab, st);
-    } else if (apply == APPLY_F) {
-        rc = launch_fused_cfg<1, APPLY_F>(a, kt, tab, st);
-    } else {
-        switch (nr) {
-            case 1: rc = launch_fused_cfg<1, APPLY_Q>(a, kt, tab, st); break;
-            case 2: rc = launch_fused_cfg<2, APPLY_Q>(a, kt, tab, st); break;
-            case 3: rc = launch_fused_cfg<3, APPLY_Q>(a, kt, tab, st); break;
-            case 4: rc = launch_fused_cfg<4, APPLY_Q>(a, kt, tab, st); break;
-            case 5: rc = launch_fused_cfg<5, APPLY_Q>(a, kt, tab, st); break;
-            case 6: rc = launch_fused_cfg<6, APPLY_Q>(a, kt, tab, st); break;
-            case 7: rc = launch_fused_cfg<7, APPLY_Q>(a, kt, tab, st); break;
-            case 8: rc = launch_fused_cfg<8, APPLY_Q>(a, kt, tab, st); break;
-            default: return fail(CDSGD_ERR_ARG, "fused step supports 1..8 ranks");
-        }
+template <typename TW>
+int launch_fused_t(int nr, int apply, const FusedArgs& a, const KeyTab& kt, const DecodeTab& tab, cudaStream_t st) {
+    if (apply == APPLY_L) return launch_fused_cfg<1, APPLY_L, TW>(a, kt, tab, st);  // W final: loc + quantize only
+    if (apply == APPLY_F) return launch_fused_cfg<1, APPLY_F, TW>(a, kt, tab, st);
+    switch (nr) {
+        case 1: return launch_fused_cfg<1, APPLY_Q, TW>(a, kt, tab, st);
+        case 2: return launch_fused_cfg<2, APPLY_Q, TW>(a, kt, tab, st);
+        case 3: return launch_fused_cfg<3, APPLY_Q, TW>(a, kt, tab, st);
+        case 4: return launch_fused_cfg<4, APPLY_Q, TW>(a, kt, tab, st);
+        case 5: return launch_fused_cfg<5, APPLY_Q, TW>(a, kt, tab, st);
+        case 6: return launch_fused_cfg<6, APPLY_Q, TW>(a, kt, tab, st);
+        case 7: return launch_fused_cfg<7, APPLY_Q, TW>(a, kt, tab, st);
+        case 8: return launch_fused_cfg<8, APPLY_Q, TW>(a, kt, tab, st);
+        default: return fail(CDSGD_ERR_ARG, "fused step supports 1..8 ranks");
     }
+}
+int launch_fused(int nr, int apply, int wdt, const FusedArgs& a, const KeyTab& kt, const DecodeTab& tab,
+                 cudaStream_t st) {
+    const int rc = wdt == CDSGD_F64 ? launch_fused_t<double>(nr, apply, a, kt, tab, st)
+                                    : launch_fused_t<float>(nr, apply, a, kt, tab, st);
     if (rc != CDSGD_OK) return rc;
     LAUNCH_CHECK();
     return CDSGD_OK;
 }
+bool wdt_ok(int wdt) { return wdt == CDSGD_F32 || wdt == CDSGD_F64; }
 }  // namespace
 
-extern "C" int cdsgd_apply_quant(const cdsgd_layout* L, float* W, const uint32_t* gathered, int32_t nr,
+extern "C" int cdsgd_apply_quant(const cdsgd_layout* L, void* W, int32_t wdt, const uint32_t* gathered, int32_t nr,
                                  int64_t stride, double alpha, double eta_g, const float* gnext, float* loc,
                                  double eta_l, uint64_t* err, uint64_t skip_below, double* gnorm, void* stream) {
     if (!(alpha > 0.0)) return fail(CDSGD_ERR_ARG, "threshold alpha must be > 0");
-    return launch_apply_quant(L, W, gathered, nr, stride, alpha, eta_g, gnext, loc, eta_l, err, skip_below, gnorm,
-                              nullptr, 0, S(stream));
+    if (!wdt_ok(wdt)) return fail(CDSGD_ERR_ARG, "weights dtype must be CDSGD_F32 or CDSGD_F64");
+    return launch_apply_quant(L, W, wdt, gathered, nr, stride, alpha, eta_g, gnext, loc, eta_l, err, skip_below,
+                              gnorm, nullptr, 0, S(stream));
 }
 
-extern "C" int cdsgd_apply_full(float* W, const float* gsum, int32_t nr, int64_t n, double eta_g,
+extern "C" int cdsgd_apply_full(void* W, int32_t wdt, const float* gsum, int32_t nr, int64_t n, double eta_g,
                                 const float* gnext, float* loc, double eta_l, const uint64_t* err,
                                 uint64_t skip_below, double* gnorm, void* stream) {
-    return launch_apply_full(W, gsum, nr, n, eta_g, gnext, loc, eta_l, err, skip_below, gnorm, S(stream));
+    if (!wdt_ok(wdt)) return fail(CDSGD_ERR_ARG, "weights dtype must be CDSGD_F32 or CDSGD_F64");
+    return launch_apply_full(W, wdt, gsum, nr, n, eta_g, gnext, loc, eta_l, err, skip_below, gnorm, S(stream));
 }
 
 extern "C" int cdsgd_fused_round(const cdsgd_layout* L, const float* grad, const double* r_in, double* r_out,
-                                 uint32_t* words, double alpha, uint64_t* err, uint64_t err_tag, float* W,
-                                 float* loc, const uint32_t* gathered, int32_t nr, int64_t stride, double eta_g,
+                                 uint32_t* words, double alpha, uint64_t* err, uint64_t err_tag, void* W,
+                                 int32_t wdt, float* loc, const uint32_t* gathered, int32_t nr, int64_t stride, double eta_g,
                                  double eta_l, uint64_t skip_below, double* gnorm, void* stream) {
     if (L == nullptr) return fail(CDSGD_ERR_ARG, "layout is NULL");
     if (!(alpha > 0.0)) return fail(CDSGD_ERR_ARG, "threshold alpha must be > 0");
@@ -594,6 +623,7 @@ extern "C" int cdsgd_fused_round(const cdsgd_layout* L, const float* grad, const
     if (nr < 1 || nr > MAX_RANKS_P2P) return fail(CDSGD_ERR_ARG, "nranks must be in [1, %d]", MAX_RANKS_P2P);
     if (L->n == 0) return CDSGD_OK;
     if (!grad || !r_in || !r_out || !words || !W || !loc) return fail(CDSGD_ERR_ARG, "NULL buffer");
+    if (!wdt_ok(wdt)) return fail(CDSGD_ERR_ARG, "weights dtype must be CDSGD_F32 or CDSGD_F64");
     FusedArgs a{};
     a.g = grad;
     a.r_in = r_in;
@@ -610,6 +640,8 @@ extern "C" int cdsgd_fused_round(const cdsgd_layout* L, const float* grad, const
     a.eta_l = static_cast<float>(eta_l);
     a.exact = alpha_exact(alpha, nr) ? 1 : 0;
     a.eta_g_d = eta_g;
+    a.eta_l_d = eta_l;
+    a.nranks = nr;
     a.inv_n_or_zero = pow2(nr) ? 1.0 / nr : 0.0;
     a.skip_below = skip_below;
     a.gnorm = gathered != nullptr ? gnorm : nullptr;
@@ -617,7 +649,7 @@ extern "C" int cdsgd_fused_round(const cdsgd_layout* L, const float* grad, const
     a.sched = nullptr;  // static tile ranges: no scheduler state shared between callers
     DecodeTab tab;
     build_tab(tab, alpha, eta_g, nr);
-    return launch_fused(nr, gathered != nullptr ? APPLY_Q : APPLY_L, a, L->tab(), tab, S(stream));
+    return launch_fused(nr, gathered != nullptr ? APPLY_Q : APPLY_L, wdt, a, L->tab(), tab, S(stream));
 }
 
 // ------------------------------------------------------------------ NCCL exchange
@@ -853,10 +885,15 @@ int reduce_ctas() {
     }();
     return v;
 }
-template <int NR, bool SUM = false>
+template <int NR, bool SUM = false, typename TW = float>
 void launch_reduce_t(const ReduceArgs& a, int64_t len, cudaStream_t C) {
-    const int grid = std::min(flat_grid(k_reduce<NR, SUM>, (len + 3) / 4), reduce_ctas());
-    launch_pdl(k_reduce<NR, SUM>, grid, THREADS, 0, C, a);
+    const int grid = std::min(flat_grid(k_reduce<NR, SUM, TW>, (len + 3) / 4), reduce_ctas());
+    launch_pdl(k_reduce<NR, SUM, TW>, grid, THREADS, 0, C, a);
+}
+template <int NR>
+void launch_reduce_w(const ReduceArgs& a, int64_t len, int wdt, cudaStream_t C) {
+    if (wdt == CDSGD_F64) launch_reduce_t<NR, false, double>(a, len, C);
+    else launch_reduce_t<NR, false, float>(a, len, C);
 }
 
 // Part of a correction round's all-reduce on the COPY ENGINES: elements [off, off + cnt)
@@ -961,12 +998,12 @@ int p2p_reduce(cdsgd_engine* E, int64_t p, cudaStream_t C) {
     for (int r = 0; r < nr; ++r) {
         a.stage[r] = E->stage_push ? at<const float>(local, E->off_stage[s]) + static_cast<int64_t>(r) * E->chunk - E->s0
                                    : at<const float>(E->peer[r], E->off_stage[s]);
-        a.Wdst[r] = at<float>(E->peer[r], E->off_W);
+        a.Wdst[r] = E->peer[r] + E->off_W;
         a.gpart_dst[r] = at<double>(E->peer[r], E->off_gpart) + s * nr + me;
         a.xa.publish[r] = at<uint64_t>(E->peer[r], E->off_gfreed) + s * nr + me;
         a.xb.publish[r] = at<uint64_t>(E->peer[r], E->off_wdone) + me;
     }
-    a.W = at<const float>(local, E->off_W);
+    a.W = local + E->off_W;
     a.s0 = E->s0;
     a.s1 = E->s1;
     a.nranks = nr;
@@ -985,13 +1022,13 @@ int p2p_reduce(cdsgd_engine* E, int64_t p, cudaStream_t C) {
     const long pi = prof_start(E, 7, C);
     const int64_t len = E->s1 - E->s0;
     switch (nr) {
-        case 2: launch_reduce_t<2>(a, len, C); break;
-        case 3: launch_reduce_t<3>(a, len, C); break;
-        case 4: launch_reduce_t<4>(a, len, C); break;
-        case 5: launch_reduce_t<5>(a, len, C); break;
-        case 6: launch_reduce_t<6>(a, len, C); break;
-        case 7: launch_reduce_t<7>(a, len, C); break;
-        case 8: launch_reduce_t<8>(a, len, C); break;
+        case 2: launch_reduce_w<2>(a, len, E->d.weights_dtype, C); break;
+        case 3: launch_reduce_w<3>(a, len, E->d.weights_dtype, C); break;
+        case 4: launch_reduce_w<4>(a, len, E->d.weights_dtype, C); break;
+        case 5: launch_reduce_w<5>(a, len, E->d.weights_dtype, C); break;
+        case 6: launch_reduce_w<6>(a, len, E->d.weights_dtype, C); break;
+        case 7: launch_reduce_w<7>(a, len, E->d.weights_dtype, C); break;
+        case 8: launch_reduce_w<8>(a, len, E->d.weights_dtype, C); break;
         default: return fail(CDSGD_ERR_ARG, "P2P correction supports 2..8 ranks");
     }
     LAUNCH_CHECK();
@@ -1033,7 +1070,7 @@ int engine_apply(cdsgd_engine* E, int64_t p, bool comp, const float* gp, const f
         if (E->xused[p & 1]) CUDA_TRY(cudaStreamWaitEvent(C, E->evX[p & 1], 0));  // reduce already ran on X
         else rc = p2p_reduce(E, p, C);
         if (rc == CDSGD_OK && gnext != nullptr)
-            rc = cdsgd_local_update(E->d.weights, CDSGD_F32, gnext, CDSGD_F32, E->d.loc, CDSGD_F32, E->L->n,
+            rc = cdsgd_local_update(E->d.weights, E->d.weights_dtype, gnext, CDSGD_F32, E->d.loc, CDSGD_F32, E->L->n,
                                     E->d.eta_local, C);
         return rc;
     }
@@ -1064,7 +1101,8 @@ int engine_apply(cdsgd_engine* E, int64_t p, bool comp, const float* gp, const f
         double* gn2 = fold ? gnorm_slot(E, p + 1) : nullptr;  // grad-norm slot of the folded correction p+1
         if (gn2 != nullptr && !gnorm_ahead(E)) CUDA_TRY(cudaMemsetAsync(gn2, 0, sizeof(double), C));
         const long pi = prof_start(E, 1, C);
-        const int rc = launch_apply_quant(E->L, E->d.weights, E->d.gathered[p & 1], nr, words_of(E), E->d.alpha,
+        const int rc = launch_apply_quant(E->L, E->d.weights, E->d.weights_dtype, E->d.gathered[p & 1], nr, words_of(E),
+                                          E->d.alpha,
                                           E->d.eta_global, gnext, loc, E->d.eta_local, E->d.err, skip_below, gn,
                                           &E->tab, E->exact, C, &x, gs, xs,
                                           E->sched != nullptr ? E->sched + 2 : nullptr,
@@ -1074,7 +1112,8 @@ int engine_apply(cdsgd_engine* E, int64_t p, bool comp, const float* gp, const f
     }
     const float* gsum = nr > 1 ? E->d.gsum[p & 1] : gp;
     const long pi = prof_start(E, 2, C);
-    const int rc = launch_apply_full(E->d.weights, gsum, nr, E->L->n, E->d.eta_global, gnext, loc, E->d.eta_local,
+    const int rc = launch_apply_full(E->d.weights, E->d.weights_dtype, gsum, nr, E->L->n, E->d.eta_global, gnext, loc,
+                                     E->d.eta_local,
                                      E->d.err, skip_below, gn, C, clr);
     prof_stop(E, pi, C);
     return rc;
@@ -1092,6 +1131,7 @@ extern "C" int cdsgd_engine_create(const cdsgd_engine_desc* d, const cdsgd_layou
     if (d->warmup_n < 0) return fail(CDSGD_ERR_ARG, "warmup_n must be >= 0");
     if (!(d->alpha > 0.0)) return fail(CDSGD_ERR_ARG, "alpha must be > 0");
     if (!(d->eta_global > 0.0) || !(d->eta_local > 0.0)) return fail(CDSGD_ERR_ARG, "learning rates must be > 0");
+    if (!wdt_ok(d->weights_dtype)) return fail(CDSGD_ERR_ARG, "weights_dtype must be CDSGD_F32 or CDSGD_F64");
     if (!d->weights || !d->loc || !d->residual[0] || !d->residual[1] || !d->gathered[0] || !d->gathered[1] || !d->err)
         return fail(CDSGD_ERR_ARG, "NULL engine buffer");
     if (d->nranks > 1 && (comm == nullptr || !d->gsum[0] || !d->gsum[1]))
@@ -1160,7 +1200,7 @@ void p2p_offsets(int32_t nranks, int64_t n, int64_t words, int64_t* off /* [14] 
     off[2] = 2 * off[1];
     off[3] = off[2] + flags;
     off[4] = off[3] + flags;
-    off[5] = off[4] + align256(4 * n);
+    off[5] = off[4] + align256(8 * n);        // W replica (sized for fp64 weights)
     off[6] = off[5] + recv;
     off[7] = off[6] + recv;
     off[8] = off[7] + flags;
@@ -1217,9 +1257,10 @@ extern "C" int cdsgd_engine_attach_p2p(cdsgd_engine* E, void* const* peer_bases,
     E->d.gathered[0] = reinterpret_cast<uint32_t*>(local + E->off_slot[0]);
     E->d.gathered[1] = reinterpret_cast<uint32_t*>(local + E->off_slot[1]);
     // the W replica moves into symmetric memory (peers store their W' shards into it)
-    float* wsym = reinterpret_cast<float*>(local + E->off_W);
+    void* wsym = local + E->off_W;
     if (wsym != E->d.weights) {
-        CUDA_TRY(cudaMemcpy(wsym, E->d.weights, 4 * E->L->n, cudaMemcpyDeviceToDevice));
+        const size_t wb = E->d.weights_dtype == CDSGD_F64 ? 8 : 4;
+        CUDA_TRY(cudaMemcpy(wsym, E->d.weights, wb * E->L->n, cudaMemcpyDeviceToDevice));
         E->d.weights = wsym;
     }
     const int64_t chunk = p2p_chunk(nranks, E->L->n);
@@ -1407,6 +1448,8 @@ extern "C" int cdsgd_engine_step(cdsgd_engine* E, const float* g, void* stream) 
         a.eta_l = static_cast<float>(E->d.eta_local);
         a.exact = E->exact;
         a.eta_g_d = E->d.eta_global;
+        a.eta_l_d = E->d.eta_local;
+        a.nranks = nr;
         a.inv_n_or_zero = pow2(nr) ? 1.0 / nr : 0.0;
         const int64_t rel = pnd - E->err_base + 1;
         a.skip_below = rel <= 0 ? 0ull : (static_cast<uint64_t>(rel) << CDSGD_INDEX_BITS);
@@ -1447,7 +1490,7 @@ extern "C" int cdsgd_engine_step(cdsgd_engine* E, const float* g, void* stream) 
         E->rlog.push_back(static_cast<int8_t>(E->rcur));
         const long pi = prof_start(E, has_pend ? 5 : 9, C);
         const int ap = !has_pend ? APPLY_L : (E->pend_comp ? APPLY_Q : APPLY_F);
-        rc = launch_fused(nr, ap, a, E->L->tab(), E->tab, C);
+        rc = launch_fused(nr, ap, E->d.weights_dtype, a, E->L->tab(), E->tab, C);
         prof_stop(E, pi, C);
         if (rc != CDSGD_OK) return rc;
         E->rcur ^= 1;
@@ -1576,7 +1619,7 @@ extern "C" int cdsgd_engine_step(cdsgd_engine* E, const float* g, void* stream) 
         } else {
             // first local round: loc_{t+1} = W_t - eta_l * g_t (engine.py:380-382, 385-391)
             const long pi = prof_start(E, 3, C);
-            rc = cdsgd_local_update(E->d.weights, CDSGD_F32, g, CDSGD_F32, E->d.loc, CDSGD_F32, E->L->n,
+            rc = cdsgd_local_update(E->d.weights, E->d.weights_dtype, g, CDSGD_F32, E->d.loc, CDSGD_F32, E->L->n,
                                     E->d.eta_local, stream);
             prof_stop(E, pi, C);
         }

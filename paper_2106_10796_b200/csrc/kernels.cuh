@@ -409,10 +409,64 @@ __device__ __forceinline__ uint32_t quant1_lean(double r, G g, double alpha, uin
 // 4-bit fields: even elements at bits 4i, odd at 4i+2 before the shift).
 constexpr int MAX_RANKS = 16;
 struct DecodeTab {
-    double mean[2 * MAX_RANKS + 1];  // (cnt*alpha)/N
-    float upd[2 * MAX_RANKS + 1];    // (float)(eta_g * mean)
-    double sq_scale;                 // (alpha/N)^2: grad-norm metric from integer sum(cnt^2)
+    double mean[2 * MAX_RANKS + 1];   // (cnt*alpha)/N
+    float upd[2 * MAX_RANKS + 1];     // (float)(eta_g * mean)       fp32 weights
+    double upd64[2 * MAX_RANKS + 1];  // eta_g * mean (fp64 product)  fp64 weights: the reference's exact update
+    double sq_scale;                  // (alpha/N)^2: grad-norm metric from integer sum(cnt^2)
 };
+
+// ---------------------------------------------------------------- weight arithmetic
+// The global weights W are fp64 (exact mode, default: the reference keeps every weight in
+// fp64, numcore.py:95, SPEC "64-bit reals internally") or fp32 (fast mode). In fp64 every
+// update is the reference's own operation sequence — W - eta*mean with the product rounded
+// once (engine.py:511) — so W is bitwise the reference's on compressed rounds and whenever
+// the round mean is exact (N = 1); the compute weights loc = fl32(W - eta_l*g) are the
+// reference's fp64 local update (engine.py:268-274) rounded once to fp32. In fp32 W is
+// rounded once per round (a random-walk drift).
+template <typename TW> struct WV;  // 4 consecutive weights of one lane
+template <> struct WV<float> { float v[4]; };
+template <> struct WV<double> { double v[4]; };
+__device__ __forceinline__ void ldw4(const float* p, int nv, WV<float>& w) {
+    const float4 t = ld_stream_m(p, nv);
+    w.v[0] = t.x; w.v[1] = t.y; w.v[2] = t.z; w.v[3] = t.w;
+}
+__device__ __forceinline__ void ldw4(const double* p, int nv, WV<double>& w) {
+    const d4 t = ld_stream_m(p, nv);
+    w.v[0] = t.x; w.v[1] = t.y; w.v[2] = t.z; w.v[3] = t.w;
+}
+template <typename TW>
+__device__ __forceinline__ void stw4(TW* p, const WV<TW>& w, int nv) {
+    st_stream_m(p, w.v[0], w.v[1], w.v[2], w.v[3], nv);
+}
+// W - eta*mean from the decode table (code count c = #plus - #minus, already offset by N)
+__device__ __forceinline__ float w_sub_tab(float w, const float* u32, const double*, int c) {
+    return __fsub_rn(w, u32[c]);
+}
+__device__ __forceinline__ double w_sub_tab(double w, const float*, const double* u64, int c) {
+    return __dsub_rn(w, u64[c]);
+}
+// W - eta*mean for a general fp64 mean (non-exact alpha decode)
+__device__ __forceinline__ float w_sub_mean(float w, double eta, double mean) {
+    return __fsub_rn(w, __double2float_rn(__dmul_rn(eta, mean)));
+}
+__device__ __forceinline__ double w_sub_mean(double w, double eta, double mean) {
+    return __dsub_rn(w, __dmul_rn(eta, mean));
+}
+// W - eta*(gsum/N): the full-precision (correction) branch, gsum the fp32 sum over ranks.
+// fp32: one fma with (float)(eta/N); fp64: the reference's mean = sum/N, W - eta*mean
+__device__ __forceinline__ float w_sub_full(float w, float s, float scale, double, double, int) {
+    return __fmaf_rn(-scale, s, w);
+}
+__device__ __forceinline__ double w_sub_full(double w, float s, float, double eta, double inv_n_or_zero, int nr) {
+    const double m = inv_n_or_zero != 0.0 ? __dmul_rn(static_cast<double>(s), inv_n_or_zero)
+                                          : __ddiv_rn(static_cast<double>(s), static_cast<double>(nr));
+    return __dsub_rn(w, __dmul_rn(eta, m));
+}
+// compute weights: W' - eta_l*g (engine.py:268-274), stored fp32
+__device__ __forceinline__ float loc_of(float w, float g, float eta_l, double) { return __fmaf_rn(-eta_l, g, w); }
+__device__ __forceinline__ float loc_of(double w, float g, float, double eta_l) {
+    return __double2float_rn(__dsub_rn(w, __dmul_rn(eta_l, static_cast<double>(g))));
+}
 
 // Counts over ranks for the 16 codes of one word position: returns packed 4-bit
 // plus/minus counters for even (field 4i) and odd (field 4i) elements, and a
@@ -461,7 +515,7 @@ __device__ __forceinline__ float* stage_at(const StageDst& s, int64_t e, int o0,
 // W' = W - eta_g*mean (engine.py:511) on fp32 W, loc = W' - eta_l*g_next (Eq. 11,
 // engine.py:385-392), optional sum(mean^2) (engine.py:521).
 struct ApplyQArgs {
-    float* W;
+    void* W;  // float* or double* (the kernel's TW)
     const uint32_t* gathered;
     int64_t stride;  // words between ranks
     const float* gnext;
@@ -478,9 +532,9 @@ struct ApplyQArgs {
     P2PArgs xs;     // staging protocol: wait gfreed, publish gready
     unsigned int* sched;  // [2] dynamic tile scheduler {next tile, CTAs done}; nullptr = static ranges
     // N=1, the round after this one is a correction whose mean is g_next itself: also apply
-    // it here, W <- fma(-fold_scale, g_next, W) after the local update (fold_scale = eta_g/1),
-    // with its grad-norm into gnorm2. 0 = off.
-    float fold_scale;
+    // it here after the local update (W - eta_g*g_next), with its grad-norm into gnorm2.
+    float fold_scale;   // fp32 weights: (float)eta_g
+    int fold;           // 1: fold on
     double* gnorm2;
     double* gclear[2];  // grad-norm ring slots to zero (see pdl_enter), nullable
 };
@@ -499,20 +553,22 @@ __device__ __forceinline__ double apply_mean_general(const uint32_t* codes, int 
 
 // K2 vector path for one tile (exact-alpha table, compile-time rank count). Tiles of ne <
 // TILE_ELEMS elements (a key's last) use masked accesses; padding codes are ignored.
-template <int NR>
-__device__ __forceinline__ void apply_vec_tile(const ApplyQArgs& a, const float* s_upd, int nr, int lane,
-                                               int64_t e0, int64_t w0, int ne, int nw, bool do_loc, int so0,
+template <int NR, typename TW>
+__device__ __forceinline__ void apply_vec_tile(const ApplyQArgs& a, const float* s_upd, const double* s_upd64, int nr,
+                                               int lane, int64_t e0, int64_t w0, int ne, int nw, bool do_loc, int so0,
                                                int64_t sbnd, int& isq, double& gsq2, uint64_t& bad_idx) {
     constexpr int R = NR > 0 ? NR : 1;
+    TW* const W = static_cast<TW*>(a.W);
     uint32_t wv[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) wv[r] = lane < nw ? ld_word(a.gathered + r * a.stride + w0 + lane) : 0u;
-    float4 wt[CHUNKS], gt[CHUNKS];
+    WV<TW> wt[CHUNKS];
+    float4 gt[CHUNKS];
 #pragma unroll
     for (int c = 0; c < CHUNKS; ++c) {
         const int64_t e = e0 + 128 * c + 4 * lane;
         const int nv = nvalid4(ne, 128 * c + 4 * lane);
-        wt[c] = ld_stream_m(a.W + e, nv);
+        ldw4(W + e, nv, wt[c]);
         if (do_loc) gt[c] = ld_stream_m(a.gnext + e, nv);
     }
 #pragma unroll
@@ -523,7 +579,7 @@ __device__ __forceinline__ void apply_vec_tile(const ApplyQArgs& a, const float*
 #pragma unroll
         for (int r = 0; r < R; ++r) count_add(cnt, __shfl_sync(FULL, wv[r], 8 * c + (lane >> 2)));
         const int jb = 4 * (lane & 3);  // first code position of this lane in the word
-        float w4[4] = {wt[c].x, wt[c].y, wt[c].z, wt[c].w};
+        WV<TW>& w4 = wt[c];
         float g4[4];
         if (do_loc) { g4[0] = gt[c].x; g4[1] = gt[c].y; g4[2] = gt[c].z; g4[3] = gt[c].w; }
         float l4[4];
@@ -531,11 +587,11 @@ __device__ __forceinline__ void apply_vec_tile(const ApplyQArgs& a, const float*
         lane_counts(cnt, lane, cq);
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-            w4[q] = __fsub_rn(w4[q], s_upd[cq[q] + nr]);
-            if (do_loc) l4[q] = __fmaf_rn(-a.eta_l, g4[q], w4[q]);
+            w4.v[q] = w_sub_tab(w4.v[q], s_upd, s_upd64, cq[q] + nr);
+            if (do_loc) l4[q] = loc_of(w4.v[q], g4[q], a.eta_l, a.eta_l_d);
             isq += cq[q] * cq[q];
-            if (a.fold_scale != 0.f) {  // N=1 correction round t+1: W_{t+2} = W_{t+1} - eta*g_{t+1}
-                w4[q] = __fmaf_rn(-a.fold_scale, g4[q], w4[q]);
+            if (a.fold) {  // N=1 correction round t+1: W_{t+2} = W_{t+1} - eta*g_{t+1} (mean = g itself)
+                w4.v[q] = w_sub_full(w4.v[q], g4[q], a.fold_scale, a.eta_g_d, 1.0, 1);
                 const double m = static_cast<double>(g4[q]);
                 gsq2 = __fma_rn(m, m, gsq2);  // (a two-chain tree measured 2 us slower)
             }
@@ -547,7 +603,7 @@ __device__ __forceinline__ void apply_vec_tile(const ApplyQArgs& a, const float*
             bad_idx = idx < bad_idx ? idx : bad_idx;
         }
         if (nv > 0) {
-            st_stream_m(a.W + e, w4[0], w4[1], w4[2], w4[3], nv);
+            stw4(W + e, w4, nv);
             if (do_loc) st_stream_m(a.loc + e, l4[0], l4[1], l4[2], l4[3], nv);
             if (a.gs.chunk != 0) st_stream_m(stage_at(a.gs, e, so0, sbnd), g4[0], g4[1], g4[2], g4[3], nv);
         }
@@ -561,19 +617,22 @@ __device__ __forceinline__ void apply_vec_tile(const ApplyQArgs& a, const float*
 // a grid of (SMs - R) CTAs leaves R whole SMs free — launched beside a correction all-reduce,
 // whose NCCL CTAs (104 KB smem, 52K registers each) cannot share an SM with this kernel.
 #ifndef CDSGD_K2_MINB
-#define CDSGD_K2_MINB (NR == 1 ? 3 : 2)
+#define CDSGD_K2_MINB (NR == 1 && sizeof(TW) == 4 ? 3 : 2)
 #endif
-template <int NR, int WIDE = 0>
+template <int NR, int WIDE = 0, typename TW = float>
 __global__ void __launch_bounds__(WIDE ? 512 : 256, WIDE ? 1 : CDSGD_K2_MINB) k_apply_quant(ApplyQArgs a, KeyTab kt, DecodeTab tab) {
     pdl_enter(a.gclear[0], a.gclear[1]);
     const bool peer_failed = p2p_wait2(a.x, a.xs);
     const bool skip = peer_failed || (a.err != nullptr && *reinterpret_cast<volatile uint64_t*>(a.err) < a.skip_below);
     __shared__ double s_mean[2 * MAX_RANKS + 1];
+    __shared__ double s_upd64[2 * MAX_RANKS + 1];
     __shared__ float s_upd[2 * MAX_RANKS + 1];
+    TW* const W = static_cast<TW*>(a.W);
     const int nr = NR > 0 ? NR : a.nranks;
     if (threadIdx.x < 2 * nr + 1) {
         s_mean[threadIdx.x] = tab.mean[threadIdx.x];
         s_upd[threadIdx.x] = tab.upd[threadIdx.x];
+        s_upd64[threadIdx.x] = tab.upd64[threadIdx.x];
     }
     __syncthreads();
     int64_t tb, te;
@@ -616,7 +675,7 @@ __global__ void __launch_bounds__(WIDE ? 512 : 256, WIDE ? 1 : CDSGD_K2_MINB) k_
             const int ne = ne64 < TILE_ELEMS ? static_cast<int>(ne64) : TILE_ELEMS;
             const int64_t nw64 = kc.w1 - w0;
             const int nw = nw64 < TILE_WORDS ? static_cast<int>(nw64) : TILE_WORDS;
-            const bool fast = NR > 0 && a.exact && aligned_to(a.W + e0, 16) &&
+            const bool fast = NR > 0 && a.exact && aligned_to(W + e0, 4 * sizeof(TW)) &&
                               (!do_loc || (aligned_to(a.gnext + e0, 16) && aligned_to(a.loc + e0, 16)));
             int so0 = 0;
             int64_t sbnd = 0;
@@ -625,7 +684,8 @@ __global__ void __launch_bounds__(WIDE ? 512 : 256, WIDE ? 1 : CDSGD_K2_MINB) k_
                 sbnd = (so0 + 1) * a.gs.chunk;
             }
             if (fast) {
-                apply_vec_tile<NR>(a, s_upd, nr, lane, e0, w0, ne, nw, do_loc, so0, sbnd, isq, gsq2, bad_idx);
+                apply_vec_tile<NR, TW>(a, s_upd, s_upd64, nr, lane, e0, w0, ne, nw, do_loc, so0, sbnd, isq, gsq2,
+                                       bad_idx);
             } else {
                 // generic path: lane l owns element 32s + l; word (2s + l/16), code l%16
                 uint32_t wv[MAX_RANKS];
@@ -641,7 +701,7 @@ __global__ void __launch_bounds__(WIDE ? 512 : 256, WIDE ? 1 : CDSGD_K2_MINB) k_
                         const int64_t e = e0 + el;
                         bool rsv = false;
                         double mean;
-                        float upd;
+                        TW wn;
                         if (a.exact) {
                             int cn = 0;
                             for (int r = 0; r < nr; ++r) {
@@ -649,19 +709,18 @@ __global__ void __launch_bounds__(WIDE ? 512 : 256, WIDE ? 1 : CDSGD_K2_MINB) k_
                                 cn += (codes[r] == 1u) - (codes[r] == 2u);
                             }
                             mean = s_mean[cn + nr];
-                            upd = s_upd[cn + nr];
+                            wn = w_sub_tab(W[e], s_upd, s_upd64, cn + nr);
                         } else {
                             mean = apply_mean_general(codes, nr, a.alpha, a.inv_n_or_zero, rsv);
-                            upd = __double2float_rn(__dmul_rn(a.eta_g_d, mean));
+                            wn = w_sub_mean(W[e], a.eta_g_d, mean);
                         }
-                        float wn = __fsub_rn(a.W[e], upd);
-                        if (do_loc) a.loc[e] = __fmaf_rn(-a.eta_l, a.gnext[e], wn);
-                        if (a.fold_scale != 0.f) {
+                        if (do_loc) a.loc[e] = loc_of(wn, a.gnext[e], a.eta_l, a.eta_l_d);
+                        if (a.fold) {
                             const float gn = a.gnext[e];
-                            wn = __fmaf_rn(-a.fold_scale, gn, wn);
+                            wn = w_sub_full(wn, gn, a.fold_scale, a.eta_g_d, 1.0, 1);
                             gsq2 = __fma_rn(static_cast<double>(gn), static_cast<double>(gn), gsq2);
                         }
-                        a.W[e] = wn;
+                        W[e] = wn;
                         if (a.gs.chunk != 0) *stage_at(a.gs, e, so0, sbnd) = a.gnext[e];
                         if (a.gnorm != nullptr) gsq = __fma_rn(mean, mean, gsq);
                         if (rsv) bad_idx = static_cast<uint64_t>(e) < bad_idx ? static_cast<uint64_t>(e) : bad_idx;
@@ -786,13 +845,15 @@ __global__ void k_unpack(const uint32_t* __restrict__ words, int64_t length, uin
 // ================================================================ K3: apply_full + elementwise
 // Correction round: W' = W - (eta_g/N)*gsum ; loc = W' - eta_l*g_next.
 struct ApplyFArgs {
-    float* W;
+    void* W;  // float* or double*
     const float* gsum;
     const float* gnext;
     float* loc;
-    float scale;   // (float)(eta_g / N)
+    float scale;   // (float)(eta_g / N)   fp32 weights
     float eta_l;
     double inv_n;  // for the grad-norm metric
+    double eta_g_d, eta_l_d, inv_n_or_zero;  // fp64 weights: mean = gsum/N, W - eta*mean
+    int nranks;
     int64_t n;
     const uint64_t* err;
     uint64_t skip_below;

@@ -50,8 +50,8 @@ __global__ void __launch_bounds__(256) k_stage(StageArgs a) {
 
 struct ReduceArgs {
     const float* stage[MAX_RANKS_P2P];  // rank r's staged g, indexed by element (mapped or local row)
-    float* Wdst[MAX_RANKS_P2P];         // rank r's W replica (mapped)
-    const float* W;                     // my W replica (read)
+    void* Wdst[MAX_RANKS_P2P];          // rank r's W replica (mapped; TW), or gsum (SUM mode, fp32)
+    const void* W;                      // my W replica (read; TW)
     int64_t s0, s1;                     // my shard [s0, s1)
     int nranks;
     double eta_g;
@@ -63,14 +63,18 @@ struct ReduceArgs {
     int ndst;                           // destinations written: Wdst[0, ndst) (0 = all NR)
 };
 
-template <int NR>
-__device__ __forceinline__ float reduce_apply1(const float (&g)[NR], float w, double eta, double inv_n, double& msq) {
+template <typename TW> __device__ __forceinline__ TW round_w(double v);
+template <> __device__ __forceinline__ float round_w<float>(double v) { return __double2float_rn(v); }
+template <> __device__ __forceinline__ double round_w<double>(double v) { return v; }
+
+template <int NR, typename TW>
+__device__ __forceinline__ TW reduce_apply1(const float (&g)[NR], TW w, double eta, double inv_n, double& msq) {
     double tot = static_cast<double>(g[0]);
 #pragma unroll
     for (int r = 1; r < NR; ++r) tot = __dadd_rn(tot, static_cast<double>(g[r]));   // engine.py:250-253
     const double mean = inv_n != 0.0 ? __dmul_rn(tot, inv_n) : __ddiv_rn(tot, static_cast<double>(NR));
     msq = __fma_rn(mean, mean, msq);
-    return __double2float_rn(__dsub_rn(static_cast<double>(w), __dmul_rn(eta, mean)));  // engine.py:511
+    return round_w<TW>(__dsub_rn(static_cast<double>(w), __dmul_rn(eta, mean)));  // engine.py:511
 }
 
 // SUM mode (p2p exchange's NCCL-free correction all-reduce): the shard's fp64 ascending
@@ -85,18 +89,39 @@ __device__ __forceinline__ float sum1(const float (&g)[NR]) {
     return __double2float_rn(tot);
 }
 
-template <int NR, bool SUM = false>
+template <int NR, bool SUM = false, typename TW = float>  // TW: W element type (SUM: fp32 gsum)
 __global__ void __launch_bounds__(256) k_reduce(ReduceArgs a) {
     pdl_enter(nullptr, nullptr);
     p2p_wait(a.xa);
+    const TW* const Wl = static_cast<const TW*>(a.W);
     const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const int64_t nth = (int64_t)gridDim.x * blockDim.x;
     const int64_t len = a.s1 - a.s0;
     const int nd = a.ndst > 0 ? a.ndst : NR;
     double msq = 0.0;
-    bool vec = SUM || aligned_to(a.W + a.s0, 16);
+    bool vec = SUM || aligned_to(Wl + a.s0, 4 * sizeof(TW));
 #pragma unroll
-    for (int r = 0; r < NR; ++r) vec = vec && aligned_to(a.stage[r] + a.s0, 16) && aligned_to(a.Wdst[r < nd ? r : 0] + a.s0, 16);
+    for (int r = 0; r < NR; ++r)
+        vec = vec && aligned_to(a.stage[r] + a.s0, 16) &&
+              aligned_to(static_cast<TW*>(a.Wdst[r < nd ? r : 0]) + a.s0, 4 * sizeof(TW));
+    // one 4-element group at element e from the loaded stage values and (non-SUM) weights
+    auto group = [&](int64_t e, const float4 (&gv)[NR], const WV<TW>& wv) {
+        float g0[NR], g1[NR], g2[NR], g3[NR];
+#pragma unroll
+        for (int r = 0; r < NR; ++r) { g0[r] = gv[r].x; g1[r] = gv[r].y; g2[r] = gv[r].z; g3[r] = gv[r].w; }
+        WV<TW> o;
+        if constexpr (SUM) {
+            o.v[0] = sum1<NR>(g0); o.v[1] = sum1<NR>(g1); o.v[2] = sum1<NR>(g2); o.v[3] = sum1<NR>(g3);
+        } else {
+            o.v[0] = reduce_apply1<NR, TW>(g0, wv.v[0], a.eta_g, a.inv_n, msq);
+            o.v[1] = reduce_apply1<NR, TW>(g1, wv.v[1], a.eta_g, a.inv_n, msq);
+            o.v[2] = reduce_apply1<NR, TW>(g2, wv.v[2], a.eta_g, a.inv_n, msq);
+            o.v[3] = reduce_apply1<NR, TW>(g3, wv.v[3], a.eta_g, a.inv_n, msq);
+        }
+#pragma unroll
+        for (int r = 0; r < NR; ++r)  // NVLink stores (every rank's replica / gsum)
+            if (r < nd) stw4(static_cast<TW*>(a.Wdst[r]) + e, o, 4);
+    };
     int64_t done = 0;
     if (vec) {
         // U float4 positions per thread per iteration, every (remote) load issued before any use
@@ -105,57 +130,25 @@ __global__ void __launch_bounds__(256) k_reduce(ReduceArgs a) {
         int64_t i = tid;
         for (; i + (U - 1) * nth < nv; i += U * nth) {
             float4 gv[U][NR];
-            float4 wv[U];
+            WV<TW> wv[U];
 #pragma unroll
             for (int u = 0; u < U; ++u) {
                 const int64_t e = a.s0 + 4 * (i + u * nth);
 #pragma unroll
                 for (int r = 0; r < NR; ++r) gv[u][r] = ld_stream(a.stage[r] + e);  // pull: NVLink loads
-                if constexpr (!SUM) wv[u] = ld_stream(a.W + e);
+                if constexpr (!SUM) ldw4(Wl + e, 4, wv[u]);
             }
 #pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const int64_t e = a.s0 + 4 * (i + u * nth);
-                float g0[NR], g1[NR], g2[NR], g3[NR];
-#pragma unroll
-                for (int r = 0; r < NR; ++r) {
-                    g0[r] = gv[u][r].x; g1[r] = gv[u][r].y; g2[r] = gv[u][r].z; g3[r] = gv[u][r].w;
-                }
-                float4 o;
-                if constexpr (SUM) {
-                    o = make_float4(sum1<NR>(g0), sum1<NR>(g1), sum1<NR>(g2), sum1<NR>(g3));
-                } else {
-                    o.x = reduce_apply1<NR>(g0, wv[u].x, a.eta_g, a.inv_n, msq);
-                    o.y = reduce_apply1<NR>(g1, wv[u].y, a.eta_g, a.inv_n, msq);
-                    o.z = reduce_apply1<NR>(g2, wv[u].z, a.eta_g, a.inv_n, msq);
-                    o.w = reduce_apply1<NR>(g3, wv[u].w, a.eta_g, a.inv_n, msq);
-                }
-#pragma unroll
-                for (int r = 0; r < NR; ++r)
-                    if (r < nd) *reinterpret_cast<float4*>(a.Wdst[r] + e) = o;  // NVLink stores
-            }
+            for (int u = 0; u < U; ++u) group(a.s0 + 4 * (i + u * nth), gv[u], wv[u]);
         }
         for (; i < nv; i += nth) {
             const int64_t e = a.s0 + 4 * i;
             float4 gv[NR];
+            WV<TW> wv;
 #pragma unroll
             for (int r = 0; r < NR; ++r) gv[r] = ld_stream(a.stage[r] + e);
-            float g0[NR], g1[NR], g2[NR], g3[NR];
-#pragma unroll
-            for (int r = 0; r < NR; ++r) { g0[r] = gv[r].x; g1[r] = gv[r].y; g2[r] = gv[r].z; g3[r] = gv[r].w; }
-            float4 o;
-            if constexpr (SUM) {
-                o = make_float4(sum1<NR>(g0), sum1<NR>(g1), sum1<NR>(g2), sum1<NR>(g3));
-            } else {
-                const float4 wv = ld_stream(a.W + e);
-                o.x = reduce_apply1<NR>(g0, wv.x, a.eta_g, a.inv_n, msq);
-                o.y = reduce_apply1<NR>(g1, wv.y, a.eta_g, a.inv_n, msq);
-                o.z = reduce_apply1<NR>(g2, wv.z, a.eta_g, a.inv_n, msq);
-                o.w = reduce_apply1<NR>(g3, wv.w, a.eta_g, a.inv_n, msq);
-            }
-#pragma unroll
-            for (int r = 0; r < NR; ++r)
-                if (r < nd) *reinterpret_cast<float4*>(a.Wdst[r] + e) = o;
+            if constexpr (!SUM) ldw4(Wl + e, 4, wv);
+            group(e, gv, wv);
         }
         done = 4 * nv;
     }
@@ -164,10 +157,12 @@ __global__ void __launch_bounds__(256) k_reduce(ReduceArgs a) {
         float g[NR];
 #pragma unroll
         for (int r = 0; r < NR; ++r) g[r] = a.stage[r][e];
-        const float o = SUM ? sum1<NR>(g) : reduce_apply1<NR>(g, a.W[e], a.eta_g, a.inv_n, msq);
+        TW o;
+        if constexpr (SUM) o = sum1<NR>(g);
+        else o = reduce_apply1<NR, TW>(g, Wl[e], a.eta_g, a.inv_n, msq);
 #pragma unroll
         for (int r = 0; r < NR; ++r)
-            if (r < nd) a.Wdst[r][e] = o;
+            if (r < nd) static_cast<TW*>(a.Wdst[r])[e] = o;
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) msq += __shfl_xor_sync(FULL, msq, o);

@@ -29,7 +29,7 @@ struct FusedArgs {
     double alpha;
     uint64_t tag;
     // apply(t-1)
-    float* W;
+    void* W;  // float* or double* (the kernel's TW)
     float* loc;
     const uint32_t* gathered;  // APPLY_Q: codes of all ranks, rank stride `stride`
     int64_t stride;
@@ -42,7 +42,8 @@ struct FusedArgs {
     // N >= 3) the tile takes the per-element path with the sequential sum of
     // engine.py:250-255 (inv_n_or_zero = 1/N for power-of-two N, else 0: divide).
     int exact;
-    double eta_g_d, inv_n_or_zero;
+    double eta_g_d, inv_n_or_zero, eta_l_d;
+    int nranks;
     uint64_t skip_below;
     double* gnorm;
     uint64_t* err;
@@ -56,13 +57,15 @@ struct FusedArgs {
 // element e0 / word w0, all loads issued before any use. A key's last tile (ne < TILE_ELEMS
 // elements) uses masked accesses; padding quantizes to code 00 (the
 // reference's zero padding of the last word, codec.py:131-143) and is never stored.
-template <int NR, int APPLY, int CH>
-__device__ __forceinline__ uint32_t fused_vec_task(const FusedArgs& a, const float* s_upd, int lane, int64_t e0,
-                                                   int64_t w0, int ne, int nw, int c0, bool a_off, bool q_off,
-                                                   uint32_t ahi, uint32_t alo, uint64_t& bad_idx, uint64_t& bad_sym,
-                                                   double& gsq, int& isq) {
+template <int NR, int APPLY, int CH, typename TW>
+__device__ __forceinline__ uint32_t fused_vec_task(const FusedArgs& a, const float* s_upd, const double* s_upd64,
+                                                   int lane, int64_t e0, int64_t w0, int ne, int nw, int c0,
+                                                   bool a_off, bool q_off, uint32_t ahi, uint32_t alo,
+                                                   uint64_t& bad_idx, uint64_t& bad_sym, double& gsq, int& isq) {
     uint32_t myword = 0;
-    float4 gv[CH], wv[CH], sv[CH];
+    TW* const W = static_cast<TW*>(a.W);
+    float4 gv[CH], sv[CH];
+    WV<TW> wv[CH];
     d4 rv[CH];
     uint32_t cw[APPLY == APPLY_Q ? NR : 1];
     if constexpr (APPLY == APPLY_Q) {
@@ -76,7 +79,7 @@ __device__ __forceinline__ uint32_t fused_vec_task(const FusedArgs& a, const flo
         const int nv = nvalid4(ne, 128 * (c0 + c) + 4 * lane);
         gv[c] = ld_stream_m(a.g + e, nv);
         rv[c] = ld_stream_m(a.r_in + e, nv);
-        wv[c] = ld_stream_m(a.W + e, nv);
+        ldw4(W + e, nv, wv[c]);
         if constexpr (APPLY == APPLY_F) sv[c] = ld_stream_m(a.gsum + e, nv);
     }
     uint32_t v[CH];
@@ -86,7 +89,7 @@ __device__ __forceinline__ uint32_t fused_vec_task(const FusedArgs& a, const flo
         const int64_t e = e0 + 128 * (c0 + c) + 4 * lane;
         const int nv = nvalid4(ne, 128 * (c0 + c) + 4 * lane);
         float g4[4] = {gv[c].x, gv[c].y, gv[c].z, gv[c].w};
-        float w4[4] = {wv[c].x, wv[c].y, wv[c].z, wv[c].w};
+        WV<TW>& w4 = wv[c];
         double r4[4] = {rv[c].x, rv[c].y, rv[c].z, rv[c].w};
         if (!a_off) {
             float l4[4];
@@ -98,8 +101,8 @@ __device__ __forceinline__ uint32_t fused_vec_task(const FusedArgs& a, const flo
                 lane_counts(cnt, lane, cq);
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
-                    w4[q] = __fsub_rn(w4[q], s_upd[cq[q] + NR]);
-                    l4[q] = __fmaf_rn(-a.eta_l, g4[q], w4[q]);
+                    w4.v[q] = w_sub_tab(w4.v[q], s_upd, s_upd64, cq[q] + NR);
+                    l4[q] = loc_of(w4.v[q], g4[q], a.eta_l, a.eta_l_d);
                     isq += cq[q] * cq[q];
                 }
                 const int jb = 4 * (lane & 3);
@@ -112,8 +115,8 @@ __device__ __forceinline__ uint32_t fused_vec_task(const FusedArgs& a, const flo
                 const float s4[4] = {sv[c].x, sv[c].y, sv[c].z, sv[c].w};
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
-                    w4[q] = __fmaf_rn(-a.scale, s4[q], w4[q]);
-                    l4[q] = __fmaf_rn(-a.eta_l, g4[q], w4[q]);
+                    w4.v[q] = w_sub_full(w4.v[q], s4[q], a.scale, a.eta_g_d, a.inv_n_or_zero, a.nranks);
+                    l4[q] = loc_of(w4.v[q], g4[q], a.eta_l, a.eta_l_d);
                     if (a.gnorm != nullptr) {
                         const double m = s4[q] * a.inv_n;
                         gsq = __fma_rn(m, m, gsq);
@@ -121,9 +124,9 @@ __device__ __forceinline__ uint32_t fused_vec_task(const FusedArgs& a, const flo
                 }
             } else {
 #pragma unroll
-                for (int q = 0; q < 4; ++q) l4[q] = __fmaf_rn(-a.eta_l, g4[q], w4[q]);
+                for (int q = 0; q < 4; ++q) l4[q] = loc_of(w4.v[q], g4[q], a.eta_l, a.eta_l_d);
             }
-            if constexpr (APPLY != APPLY_L) st_stream_m(a.W + e, w4[0], w4[1], w4[2], w4[3], nv);
+            if constexpr (APPLY != APPLY_L) stw4(W + e, w4, nv);
             st_stream_m(a.loc + e, l4[0], l4[1], l4[2], l4[3], nv);
         }
         if (!q_off) {
@@ -167,10 +170,12 @@ __device__ __forceinline__ uint32_t fused_vec_task(const FusedArgs& a, const flo
 // tile issued first), two 256-thread CTAs per SM, dynamic tile scheduling.
 // CH = chunks of 128 elements per task: 4 (a whole tile) for large layouts, 1 for small
 // ones (ResNet-20-sized), where 4x more warps in flight beat the per-tile latency chain.
-template <int NR, int APPLY, int CH = CHUNKS>
+template <int NR, int APPLY, int CH = CHUNKS, typename TW = float>
 __global__ void __launch_bounds__(256, 2) k_fused_ldg(FusedArgs a, KeyTab kt, DecodeTab tab) {
     constexpr int SPL = CHUNKS / CH;  // tasks per tile
     __shared__ float s_upd[2 * MAX_RANKS + 1];
+    __shared__ double s_upd64[2 * MAX_RANKS + 1];
+    TW* const W = static_cast<TW*>(a.W);
     pdl_enter(a.gclear[0], a.gclear[1]);
     const bool peer_failed = p2p_wait2(a.xq, a.xa);
     const uint64_t e0v = a.err != nullptr ? *reinterpret_cast<volatile uint64_t*>(a.err) : ~0ull;
@@ -179,7 +184,10 @@ __global__ void __launch_bounds__(256, 2) k_fused_ldg(FusedArgs a, KeyTab kt, De
     // (the reported index stays the first non-finite element, codec.py:182-185)
     const bool q_off = e0v < a.tag || peer_failed;
     const bool a_off = e0v < a.skip_below || peer_failed;
-    if (APPLY == APPLY_Q && threadIdx.x < 2 * NR + 1) s_upd[threadIdx.x] = tab.upd[threadIdx.x];
+    if (APPLY == APPLY_Q && threadIdx.x < 2 * NR + 1) {
+        s_upd[threadIdx.x] = tab.upd[threadIdx.x];
+        s_upd64[threadIdx.x] = tab.upd64[threadIdx.x];
+    }
     __syncthreads();
     const int lane = threadIdx.x & 31;
     const uint32_t ahi = static_cast<uint32_t>(__double2hiint(a.alpha));
@@ -235,13 +243,13 @@ __global__ void __launch_bounds__(256, 2) k_fused_ldg(FusedArgs a, KeyTab kt, De
             const int64_t nw64 = cc.w1 - w0;
             const int nw = nw64 < TILE_WORDS ? static_cast<int>(nw64) : TILE_WORDS;
             const bool fast = aligned_to(a.g + e0, 16) && aligned_to(a.r_in + e0, 32) &&
-                              aligned_to(a.r_out + e0, 32) && aligned_to(a.W + e0, 16) && aligned_to(a.loc + e0, 16) &&
+                              aligned_to(a.r_out + e0, 32) && aligned_to(W + e0, 4 * sizeof(TW)) && aligned_to(a.loc + e0, 16) &&
                               (APPLY != APPLY_F || aligned_to(a.gsum + e0, 16)) && (APPLY != APPLY_Q || a.exact);
             if (!fast && c0 != 0) continue;  // misaligned tiles: one task does the whole tile
             uint32_t myword = 0;
             if (fast) {
-                myword = fused_vec_task<NR, APPLY, CH>(a, s_upd, lane, e0, w0, ne, nw, c0, a_off, q_off, ahi, alo,
-                                                       bad_idx, bad_sym, gsq, isq);
+                myword = fused_vec_task<NR, APPLY, CH, TW>(a, s_upd, s_upd64, lane, e0, w0, ne, nw, c0, a_off, q_off,
+                                                           ahi, alo, bad_idx, bad_sym, gsq, isq);
             } else {
                 uint32_t cw[APPLY == APPLY_Q ? NR : 1];
                 if constexpr (APPLY == APPLY_Q) {
@@ -268,27 +276,27 @@ __global__ void __launch_bounds__(256, 2) k_fused_ldg(FusedArgs a, KeyTab kt, De
                         const int64_t e = e0 + el;
                         const float gval = a.g[e];
                         if (!a_off) {
-                            float wn;
+                            TW wn;
                             if constexpr (APPLY == APPLY_Q) {
                                 if (a.exact) {
-                                    wn = __fsub_rn(a.W[e], s_upd[cn + NR]);
+                                    wn = w_sub_tab(W[e], s_upd, s_upd64, cn + NR);
                                     isq += cn * cn;
                                 } else {  // sequential ascending-rank fp64 sum, as K2's generic path
                                     bool r2 = false;
                                     const double mean = apply_mean_general(cds, NR, a.alpha, a.inv_n_or_zero, r2);
-                                    wn = __fsub_rn(a.W[e], __double2float_rn(__dmul_rn(a.eta_g_d, mean)));
+                                    wn = w_sub_mean(W[e], a.eta_g_d, mean);
                                     if (a.gnorm != nullptr) gsq = __fma_rn(mean, mean, gsq);
                                 }
                                 if (rsv) bad_sym = static_cast<uint64_t>(e) < bad_sym ? static_cast<uint64_t>(e) : bad_sym;
                             } else if constexpr (APPLY == APPLY_F) {
                                 const float sv1 = a.gsum[e];
-                                wn = __fmaf_rn(-a.scale, sv1, a.W[e]);
+                                wn = w_sub_full(W[e], sv1, a.scale, a.eta_g_d, a.inv_n_or_zero, a.nranks);
                                 if (a.gnorm != nullptr) { const double mm = sv1 * a.inv_n; gsq = __fma_rn(mm, mm, gsq); }
                             } else {
-                                wn = a.W[e];
+                                wn = W[e];
                             }
-                            if constexpr (APPLY != APPLY_L) a.W[e] = wn;
-                            a.loc[e] = __fmaf_rn(-a.eta_l, gval, wn);
+                            if constexpr (APPLY != APPLY_L) W[e] = wn;
+                            a.loc[e] = loc_of(wn, gval, a.eta_l, a.eta_l_d);
                         }
                         if (!q_off) {
                             double o;

@@ -244,19 +244,21 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
 }
 
 // ================================================================ K3 (TMA)
-template <int WARPS, int S>
+template <int WARPS, int S, typename TW = float>
 struct ApplyFSmem {
-    static constexpr int SLOT = 3 * TILE_ELEMS * 4;
+    static constexpr int WB = TILE_ELEMS * static_cast<int>(sizeof(TW));
+    static constexpr int SLOT = WB + 2 * TILE_ELEMS * 4;  // W | gsum | g_next
     static constexpr int WARP = S * SLOT;
     static constexpr int BYTES = WARPS * WARP + WARPS * S * 8;
 };
 
-template <int WARPS, int S>
+template <int WARPS, int S, typename TW = float>
 __global__ void __launch_bounds__(WARPS * 32, 1) k_apply_full_tma(ApplyFArgs a) {
-    using SM = ApplyFSmem<WARPS, S>;
+    using SM = ApplyFSmem<WARPS, S, TW>;
     extern __shared__ __align__(128) unsigned char smem[];
     pdl_enter(a.gclear[0], a.gclear[1]);
     if (a.err != nullptr && *reinterpret_cast<volatile const uint64_t*>(a.err) < a.skip_below) return;
+    TW* const W = static_cast<TW*>(a.W);
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     unsigned char* ring = smem + warp * SM::WARP;
@@ -275,15 +277,15 @@ __global__ void __launch_bounds__(WARPS * 32, 1) k_apply_full_tma(ApplyFArgs a) 
         uint32_t staged = 0, phase = 0;
         auto issue = [&](int64_t ti, int slot) {
             const int64_t e0 = ti * TILE_ELEMS;
-            const bool ok = e0 + TILE_ELEMS <= a.n && aligned_to(a.W + e0, 16) && aligned_to(a.gsum + e0, 16) &&
+            const bool ok = e0 + TILE_ELEMS <= a.n && aligned_to(W + e0, 4 * sizeof(TW)) && aligned_to(a.gsum + e0, 16) &&
                             (!do_loc || (aligned_to(a.gnext + e0, 16) && aligned_to(a.loc + e0, 16)));
             if (ok) {
                 if (lane == 0) {
                     unsigned char* sl = ring + slot * SM::SLOT;
-                    tma::arrive_expect_tx(&bars[slot], TILE_ELEMS * 4 * (do_loc ? 3 : 2));
-                    tma::bulk_g2s(sl, a.W + e0, TILE_ELEMS * 4, &bars[slot]);
-                    tma::bulk_g2s(sl + TILE_ELEMS * 4, a.gsum + e0, TILE_ELEMS * 4, &bars[slot]);
-                    if (do_loc) tma::bulk_g2s(sl + 2 * TILE_ELEMS * 4, a.gnext + e0, TILE_ELEMS * 4, &bars[slot]);
+                    tma::arrive_expect_tx(&bars[slot], SM::WB + TILE_ELEMS * 4 * (do_loc ? 2 : 1));
+                    tma::bulk_g2s(sl, W + e0, SM::WB, &bars[slot]);
+                    tma::bulk_g2s(sl + SM::WB, a.gsum + e0, TILE_ELEMS * 4, &bars[slot]);
+                    if (do_loc) tma::bulk_g2s(sl + SM::WB + TILE_ELEMS * 4, a.gnext + e0, TILE_ELEMS * 4, &bars[slot]);
                 }
                 staged |= 1u << slot;
             } else {
@@ -301,33 +303,35 @@ __global__ void __launch_bounds__(WARPS * 32, 1) k_apply_full_tma(ApplyFArgs a) 
             if (staged & (1u << slot)) {
                 tma::wait(&bars[slot], (phase >> slot) & 1u);
                 phase ^= 1u << slot;
-                const float* sl = reinterpret_cast<const float*>(ring + slot * SM::SLOT);
+                const TW* sw = reinterpret_cast<const TW*>(ring + slot * SM::SLOT);
+                const float* sl = reinterpret_cast<const float*>(ring + slot * SM::SLOT + SM::WB);
 #pragma unroll
                 for (int c = 0; c < CHUNKS; ++c) {
                     const int64_t e = e0 + 128 * c + 4 * lane;
-                    float w4[4], s4[4], g4[4];
-                    tma::lds4(sl + 128 * c, lane, w4);
-                    tma::lds4(sl + TILE_ELEMS + 128 * c, lane, s4);
-                    if (do_loc) tma::lds4(sl + 2 * TILE_ELEMS + 128 * c, lane, g4);
+                    TW w4[4];
+                    float s4[4], g4[4];
+                    tma::lds4(sw + 128 * c, lane, w4);
+                    tma::lds4(sl + 128 * c, lane, s4);
+                    if (do_loc) tma::lds4(sl + TILE_ELEMS + 128 * c, lane, g4);
 #pragma unroll
                     for (int q = 0; q < 4; ++q) {
-                        w4[q] = __fmaf_rn(-a.scale, s4[q], w4[q]);
-                        if (do_loc) g4[q] = __fmaf_rn(-a.eta_l, g4[q], w4[q]);
+                        w4[q] = w_sub_full(w4[q], s4[q], a.scale, a.eta_g_d, a.inv_n_or_zero, a.nranks);
+                        if (do_loc) g4[q] = loc_of(w4[q], g4[q], a.eta_l, a.eta_l_d);
                         if (a.gnorm != nullptr) {
                             const double m = s4[q] * a.inv_n;
                             gsq = __fma_rn(m, m, gsq);
                         }
                     }
-                    st_stream(a.W + e, w4[0], w4[1], w4[2], w4[3]);
+                    st_stream(W + e, w4[0], w4[1], w4[2], w4[3]);
                     if (do_loc) st_stream(a.loc + e, g4[0], g4[1], g4[2], g4[3]);
                 }
             } else {
                 const int64_t e1 = e0 + TILE_ELEMS < a.n ? e0 + TILE_ELEMS : a.n;
                 for (int64_t i = e0 + lane; i < e1; i += 32) {
                     const float s = a.gsum[i];
-                    const float wn = __fmaf_rn(-a.scale, s, a.W[i]);
-                    a.W[i] = wn;
-                    if (do_loc) a.loc[i] = __fmaf_rn(-a.eta_l, a.gnext[i], wn);
+                    const TW wn = w_sub_full(W[i], s, a.scale, a.eta_g_d, a.inv_n_or_zero, a.nranks);
+                    W[i] = wn;
+                    if (do_loc) a.loc[i] = loc_of(wn, a.gnext[i], a.eta_l, a.eta_l_d);
                     if (a.gnorm != nullptr) {
                         const double m = s * a.inv_n;
                         gsq = __fma_rn(m, m, gsq);

@@ -74,9 +74,14 @@ class CDSGDModule:
             p.grad = v
 
     def _load(self, flat: torch.Tensor) -> None:
-        # one multi-tensor launch instead of a copy per parameter (ResNet-50: 161 launches)
+        # one multi-tensor launch instead of a copy per parameter (ResNet-50: 161 launches);
+        # fp64 global weights (exact mode: warm-up rounds, flush) are rounded to fp32 first
+        if flat.dtype != torch.float32:
+            views = self._make_views(flat.to(torch.float32))  # a temporary: not cached
+        else:
+            views = self._views(flat)
         with torch.no_grad():
-            torch._foreach_copy_(self.params, self._views(flat))
+            torch._foreach_copy_(self.params, views)
 
     @property
     def t(self) -> int:

@@ -61,6 +61,7 @@ class CDSGDWorker:
         device=None,
         exchange: str = "p2p",
         group=None,
+        weights: str = "f64",
     ):
         if not torch.cuda.is_available():
             raise _lib.LibraryError("CDSGDWorker needs a CUDA device (no CPU fallback)")
@@ -81,9 +82,13 @@ class CDSGDWorker:
         w0 = init_weights if isinstance(init_weights, torch.Tensor) else torch.from_numpy(np.asarray(init_weights))
         if w0.numel() != n:
             raise ConfigError(f"initial weights have {w0.numel()} elements, layout needs {n}")
+        if weights not in _lib.WEIGHTS:
+            raise ConfigError(f"weights must be 'f64' (exact) or 'f32' (fast), got {weights!r}")
+        self.weights_dtype = weights
+        wt = torch.float64 if weights == "f64" else torch.float32
         with torch.cuda.device(dev):
-            self.W = w0.reshape(-1).to(device=dev, dtype=torch.float32).clone()
-            self.loc = self.W.clone()
+            self.W = w0.reshape(-1).to(device=dev, dtype=wt).clone()
+            self.loc = w0.reshape(-1).to(device=dev, dtype=torch.float32).clone()
             self.residuals = [torch.zeros(n, dtype=torch.float64, device=dev), torch.empty(n, dtype=torch.float64, device=dev)]
             self.gathered = [torch.zeros(self.world * nw, dtype=torch.int32, device=dev).view(torch.uint32) for _ in range(2)]
             self.gsum = [torch.empty(n, dtype=torch.float32, device=dev) for _ in range(2)] if self.world > 1 else [None, None]
@@ -99,6 +104,7 @@ class CDSGDWorker:
             d.force_compress = int(force_compress)
             d.bypass_local = int(bypass_local)
             d.gnorm_ring = self.gnorm_ring
+            d.weights_dtype = _lib.WEIGHTS[weights]
             d.alpha = float(hp.alpha)
             d.eta_global = float(hp.eta_global)
             d.eta_local = float(hp.local_lr)
@@ -155,7 +161,8 @@ class CDSGDWorker:
         _lib.check(lib.cdsgd_engine_attach_p2p(self._eng, arr, self.world, int(exact)), "cdsgd_engine_attach_p2p")
         # the engine moved the W replica into the symmetric buffer (peers write W' shards into it),
         # and the code slots live there too (slot 0 at offset 0, slot 1 at the next 256-B boundary)
-        self.W = self._symm[w_off:w_off + 4 * n].view(torch.float32)
+        es = self.W.element_size()
+        self.W = self._symm[w_off:w_off + es * n].view(self.W.dtype)
         slot = (self.world * nw * 4 + 255) // 256 * 256
         self.gathered = [self._symm[i * slot:i * slot + self.world * nw * 4].view(torch.uint32) for i in range(2)]
         torch.cuda.synchronize(self.device)
@@ -178,7 +185,9 @@ class CDSGDWorker:
 
     @property
     def weights(self) -> torch.Tensor:
-        """Global weights replica (W_t once every started round is applied, see flush())."""
+        """Global weights replica (W_t once every started round is applied, see flush()):
+        fp64 in the exact mode (bitwise the reference's W on compressed rounds), fp32 in the
+        fast mode."""
         return self.W
 
     def compute_weights(self) -> torch.Tensor:

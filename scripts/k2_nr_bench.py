@@ -46,7 +46,7 @@ def main():
     for nr in (1, 2, 4, 8):
         cw = codes(nw, nr)
         for tag, gp in (("loc", True), ("noloc", False)):
-            fn = lambda: lib.cdsgd_apply_quant(h, W.data_ptr(), cw.data_ptr(), nr, nw, 0.5, 0.1,
+            fn = lambda: lib.cdsgd_apply_quant(h, W.data_ptr(), 0, cw.data_ptr(), nr, nw, 0.5, 0.1,
                                                g.data_ptr() if gp else None, loc.data_ptr() if gp else None, 0.4,
                                                None, 0, gn.data_ptr(), st)
             out[f"nr{nr}_{tag}"] = round(timeit(fn), 1)
@@ -65,7 +65,7 @@ def main():
         cs = buf[4 * n: 4 * n + 16 * nw].view(torch.int32)
         cs.copy_(codes(nw, 4))
         for tag, Wp, cp in (("symmW_symmC", Ws, cs), ("symmW_regC", Ws, codes(nw, 4)), ("regW_symmC", W, cs)):
-            fn = lambda: lib.cdsgd_apply_quant(h, Wp.data_ptr(), cp.data_ptr(), 4, nw, 0.5, 0.1, g.data_ptr(),
+            fn = lambda: lib.cdsgd_apply_quant(h, Wp.data_ptr(), 0, cp.data_ptr(), 4, nw, 0.5, 0.1, g.data_ptr(),
                                                loc.data_ptr(), 0.4, None, 0, gn.data_ptr(), st)
             out[f"nr4_loc_{tag}"] = round(timeit(fn), 1)
         dist.destroy_process_group()

@@ -66,11 +66,11 @@ def main():
     W = torch.randn(n, device="cuda")
     gs = torch.randn(n, device="cuda")
     loc = torch.empty(n, device="cuda")
-    us = timeit(lambda: lib.cdsgd_apply_full(W.data_ptr(), gs.data_ptr(), 1, n, 0.1, g.data_ptr(), loc.data_ptr(),
+    us = timeit(lambda: lib.cdsgd_apply_full(W.data_ptr(), 0, gs.data_ptr(), 1, n, 0.1, g.data_ptr(), loc.data_ptr(),
                                              0.4, None, 0, None, st))
     out["apply_full"] = {"us": us, "GBs": 20 * n / us / 1e3}
     gath = torch.zeros(nw, dtype=torch.int32, device="cuda")
-    us = timeit(lambda: lib.cdsgd_apply_quant(h, W.data_ptr(), gath.data_ptr(), 1, nw, 0.5, 0.1, g.data_ptr(),
+    us = timeit(lambda: lib.cdsgd_apply_quant(h, W.data_ptr(), 0, gath.data_ptr(), 1, nw, 0.5, 0.1, g.data_ptr(),
                                               loc.data_ptr(), 0.4, None, 0, None, st))
     out["apply_quant_n1"] = {"us": us, "GBs": (16 * n + 4 * nw) / us / 1e3}
     print(json.dumps({k: {kk: round(vv, 1) for kk, vv in v.items()} for k, v in out.items()}, indent=1))

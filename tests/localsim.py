@@ -31,7 +31,7 @@ ALGOS = ("ssgd", "lusgd", "bitsgd", "cdsgd")
 
 class LocalSim:
     def __init__(self, layout, n_workers, w0, *, algo="cdsgd", k=4, alpha=0.5, eta_g=0.1, eta_l=0.4, warmup=0,
-                 fused=True):
+                 fused=True, weights="f64"):
         self.lib = _lib.lib()
         self.layout, self.N, self.k, self.alpha = layout, n_workers, k, alpha
         self.eta_g, self.eta_l, self.warm, self.algo = eta_g, eta_l, warmup, algo
@@ -42,9 +42,11 @@ class LocalSim:
         self.n, self.nw = n, nw
         self.lay = layout.handle().ptr
         dev = torch.device("cuda")
-        w0 = torch.as_tensor(np.asarray(w0, dtype=np.float32), device=dev)
-        self.W = [w0.clone() for _ in range(n_workers)]
-        self.loc = [w0.clone() for _ in range(n_workers)]
+        self.wdt = _lib.WEIGHTS[weights]
+        wt = torch.float64 if weights == "f64" else torch.float32
+        w0 = torch.as_tensor(np.asarray(w0), device=dev)
+        self.W = [w0.to(wt).clone() for _ in range(n_workers)]
+        self.loc = [w0.to(torch.float32).clone() for _ in range(n_workers)]
         self.res = [[torch.zeros(n, dtype=torch.float64, device=dev), torch.empty(n, dtype=torch.float64, device=dev)]
                     for _ in range(n_workers)]
         self.rcur = [0] * n_workers
@@ -97,7 +99,7 @@ class LocalSim:
         c = self.rcur[w]
         _lib.check(self.lib.cdsgd_fused_round(
             self.lay, g.data_ptr(), r[c].data_ptr(), r[c ^ 1].data_ptr(), slot.data_ptr() + 4 * w * self.nw,
-            self.alpha, self.err[w].data_ptr(), 0, self.W[w].data_ptr(), self.loc[w].data_ptr(),
+            self.alpha, self.err[w].data_ptr(), 0, self.W[w].data_ptr(), self.wdt, self.loc[w].data_ptr(),
             gathered.data_ptr() if gathered is not None else None, self.N, self.nw, self.eta_g, self.eta_l, 0,
             gnorm.data_ptr() if gnorm is not None else None, self._st()), "fused_round")
         self.rcur[w] ^= 1
@@ -107,11 +109,13 @@ class LocalSim:
         gp = gnext.data_ptr() if gnext is not None else None
         gn = gnorm.data_ptr() if gnorm is not None else None
         if comp:
-            _lib.check(self.lib.cdsgd_apply_quant(self.lay, self.W[w].data_ptr(), self.gathered[p & 1].data_ptr(),
+            _lib.check(self.lib.cdsgd_apply_quant(self.lay, self.W[w].data_ptr(), self.wdt,
+                                                  self.gathered[p & 1].data_ptr(),
                                                   self.N, self.nw, self.alpha, self.eta_g, gp, loc, self.eta_l,
                                                   self.err[w].data_ptr(), 0, gn, self._st()), "apply_quant")
         else:
-            _lib.check(self.lib.cdsgd_apply_full(self.W[w].data_ptr(), self.gsum[p & 1].data_ptr(), self.N, self.n,
+            _lib.check(self.lib.cdsgd_apply_full(self.W[w].data_ptr(), self.wdt, self.gsum[p & 1].data_ptr(), self.N,
+                                                 self.n,
                                                  self.eta_g, gp, loc, self.eta_l, None, 0, gn, self._st()),
                        "apply_full")
 
@@ -154,7 +158,7 @@ class LocalSim:
                     kinds.append("K2" if pend[1] else "K3")
                 else:
                     for w in range(self.N):
-                        _lib.check(self.lib.cdsgd_local_update(self.W[w].data_ptr(), _lib.F32, grads[w].data_ptr(),
+                        _lib.check(self.lib.cdsgd_local_update(self.W[w].data_ptr(), self.wdt, grads[w].data_ptr(),
                                                                _lib.F32, self.loc[w].data_ptr(), _lib.F32, self.n,
                                                                self.eta_l, self._st()), "local_update")
                     kinds.append("LU")

@@ -181,11 +181,11 @@ def local_sim(layout, sizes, E, name):
                 _lib.check(lib.cdsgd_quantize(lay, grads[w].data_ptr(), _lib.F32, res[w].data_ptr(), spare.data_ptr(),
                                               gathered.data_ptr() + 4 * w * nw, alpha, err.data_ptr(), 0, st))
                 res[w], spare = spare, res[w]
-            _lib.check(lib.cdsgd_apply_quant(lay, W.data_ptr(), gathered.data_ptr(), nwk, nw, alpha, eta_g, None, None,
+            _lib.check(lib.cdsgd_apply_quant(lay, W.data_ptr(), _lib.F32, gathered.data_ptr(), nwk, nw, alpha, eta_g, None, None,
                                              eta_l, err.data_ptr(), 0, None, st))
         else:
             gsum = torch.stack(grads).sum(0)  # fp32 sum, stands in for ncclAllReduce
-            _lib.check(lib.cdsgd_apply_full(W.data_ptr(), gsum.data_ptr(), nwk, n, eta_g, None, None, eta_l, None, 0,
+            _lib.check(lib.cdsgd_apply_full(W.data_ptr(), _lib.F32, gsum.data_ptr(), nwk, n, eta_g, None, None, eta_l, None, 0,
                                              None, st))
         orc.step([E[p + "grads"][t, w] for w in range(nwk)])
         np.testing.assert_allclose(W.cpu().numpy(), E[p + "weights_after"][t], rtol=RTOL, atol=ATOL,
@@ -221,7 +221,7 @@ def test_apply_quant_fused_local_update(pkg):
         gns = torch.zeros(1, dtype=torch.float64, device="cuda")
         gath = torch.from_numpy(packed.view(np.int32)).cuda().view(torch.uint32)
         err = torch.full((2,), -1, dtype=torch.int64, device="cuda")
-        _lib.check(lib.cdsgd_apply_quant(layout.handle().ptr, Wd.data_ptr(), gath.data_ptr(), nwk, nw, 0.5, 0.1,
+        _lib.check(lib.cdsgd_apply_quant(layout.handle().ptr, Wd.data_ptr(), _lib.F32, gath.data_ptr(), nwk, nw, 0.5, 0.1,
                                          gd.data_ptr(), loc.data_ptr(), 0.4, err.data_ptr(), 0, gns.data_ptr(),
                                          torch.cuda.current_stream().cuda_stream))
         deq = [O.dequantize_layout(packed[w * nw:(w + 1) * nw], 0.5, layout.lengths) for w in range(nwk)]
@@ -237,7 +237,7 @@ def test_apply_quant_fused_local_update(pkg):
     words[3] = 3 << 10  # element 16*3 + 5
     Wd = torch.zeros(600, device="cuda")
     err = torch.full((2,), -1, dtype=torch.int64, device="cuda")
-    _lib.check(lib.cdsgd_apply_quant(layout.handle().ptr, Wd.data_ptr(), words.data_ptr(), 1, layout.n_words, 0.5, 0.1,
+    _lib.check(lib.cdsgd_apply_quant(layout.handle().ptr, Wd.data_ptr(), _lib.F32, words.data_ptr(), 1, layout.n_words, 0.5, 0.1,
                                      None, None, 0.4, err.data_ptr(), 0, None, torch.cuda.current_stream().cuda_stream))
     assert int(err[1].item()) == 16 * 3 + 5
 

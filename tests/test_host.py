@@ -27,7 +27,7 @@ def test_library_exports_every_header_symbol():
     for s in syms:
         assert hasattr(lib, s), s
     assert set(syms) == set(_lib.EXPORTED_SYMBOLS)
-    assert lib.cdsgd_abi_version() == 1
+    assert lib.cdsgd_abi_version() == _lib.ABI_VERSION == 2
 
 
 def test_library_is_sm100a():
