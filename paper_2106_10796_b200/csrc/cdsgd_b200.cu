@@ -559,15 +559,16 @@ int launch_apply_full(void* W, int wdt, const float* gsum, int nr, int64_t n, do
 // Fused apply(t-1) + quantize(t), register-staged (measured faster than a TMA-ring variant).
 template <int NR, int AP, typename TW>
 int launch_fused_cfg(const FusedArgs& a, const KeyTab& kt, const DecodeTab& tab, cudaStream_t st) {
+    constexpr int CHL = sizeof(TW) == 8 ? CDSGD_F64_CH : CHUNKS;  // chunks per task on large layouts
     // fewer than 2 whole-tile tasks per resident warp: split tiles into chunk tasks
     const int64_t warps =
-        static_cast<int64_t>(resident_blocks(k_fused_ldg<NR, AP, CHUNKS, TW>, THREADS)) * WARPS_PER_BLOCK;
+        static_cast<int64_t>(resident_blocks(k_fused_ldg<NR, AP, CHL, TW>, THREADS)) * WARPS_PER_BLOCK;
     if (kt.ntiles < 2 * warps)
         launch_pdl(k_fused_ldg<NR, AP, 1, TW>, tile_grid(k_fused_ldg<NR, AP, 1, TW>, kt.ntiles * CHUNKS), THREADS, 0, st,
                    a, kt, tab);
     else
-        launch_pdl(k_fused_ldg<NR, AP, CHUNKS, TW>, tile_grid(k_fused_ldg<NR, AP, CHUNKS, TW>, kt.ntiles), THREADS, 0,
-                   st, a, kt, tab);
+        launch_pdl(k_fused_ldg<NR, AP, CHL, TW>, tile_grid(k_fused_ldg<NR, AP, CHL, TW>, kt.ntiles * (CHUNKS / CHL)),
+                   THREADS, 0, st, a, kt, tab);
     return CDSGD_OK;
 }
 template <typename TW>

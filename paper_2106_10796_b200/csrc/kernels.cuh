@@ -196,6 +196,25 @@ __device__ __forceinline__ uint64_t warp_min_u64(uint64_t v) {
     return v;
 }
 
+// CTA-wide sum of one double per thread into *dst with ONE atomic per CTA (every thread of
+// the CTA must call it). Per-warp atomics on one address serialise at L2: ~2,400 of them
+// per launch on small layouts, a visible share of a few-microsecond kernel.
+__device__ __forceinline__ void block_atomic_add(double v, double* dst) {
+    __shared__ double s_part[32];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+    const int warp = threadIdx.x >> 5, nwarp = (blockDim.x + 31) >> 5;
+    __syncthreads();  // s_part may still be read by a previous call
+    if ((threadIdx.x & 31) == 0) s_part[warp] = v;
+    __syncthreads();
+    if (warp == 0) {
+        double t = (threadIdx.x < nwarp) ? s_part[threadIdx.x] : 0.0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(FULL, t, o);
+        if (threadIdx.x == 0 && t != 0.0) atomicAdd(dst, t);
+    }
+}
+
 // ================================================================ peer exchange (P2P over NVLink)
 // Fused exchange protocol (see cdsgd_b200.cu, engine): K1 of round t stores every
 // packed word straight into each peer's gathered slot (NVLink stores through
@@ -553,7 +572,7 @@ __device__ __forceinline__ double apply_mean_general(const uint32_t* codes, int 
 
 // K2 vector path for one tile (exact-alpha table, compile-time rank count). Tiles of ne <
 // TILE_ELEMS elements (a key's last) use masked accesses; padding codes are ignored.
-template <int NR, typename TW>
+template <int NR, typename TW, bool FULL>  // FULL: whole tile, unmasked accesses (see fused_vec_task)
 __device__ __forceinline__ void apply_vec_tile(const ApplyQArgs& a, const float* s_upd, const double* s_upd64, int nr,
                                                int lane, int64_t e0, int64_t w0, int ne, int nw, bool do_loc, int so0,
                                                int64_t sbnd, int& isq, double& gsq2, uint64_t& bad_idx) {
@@ -567,14 +586,14 @@ __device__ __forceinline__ void apply_vec_tile(const ApplyQArgs& a, const float*
 #pragma unroll
     for (int c = 0; c < CHUNKS; ++c) {
         const int64_t e = e0 + 128 * c + 4 * lane;
-        const int nv = nvalid4(ne, 128 * c + 4 * lane);
+        const int nv = FULL ? 4 : nvalid4(ne, 128 * c + 4 * lane);
         ldw4(W + e, nv, wt[c]);
         if (do_loc) gt[c] = ld_stream_m(a.gnext + e, nv);
     }
 #pragma unroll
     for (int c = 0; c < CHUNKS; ++c) {
         const int64_t e = e0 + 128 * c + 4 * lane;
-        const int nv = nvalid4(ne, 128 * c + 4 * lane);
+        const int nv = FULL ? 4 : nvalid4(ne, 128 * c + 4 * lane);
         Counts cnt{0u, 0u, 0u, 0u, 0u};
 #pragma unroll
         for (int r = 0; r < R; ++r) count_add(cnt, __shfl_sync(FULL, wv[r], 8 * c + (lane >> 2)));
@@ -646,7 +665,9 @@ __global__ void __launch_bounds__(WIDE ? 512 : 256, WIDE ? 1 : CDSGD_K2_MINB) k_
     const int64_t nwarps = (int64_t)gridDim.x * blockDim.x / 32;
     const unsigned CLAIM = kt.ntiles < 4 * nwarps ? 1u : 2u;
     const int64_t tail_from = kt.ntiles - nwarps;  // single-tile claims from here on
-    const bool dyn = a.sched != nullptr;
+    // one wave of tasks (small layouts): each warp takes its own, no ticket and no end-of-launch
+    // ticket reset (a fence + atomic per CTA on one counter)
+    const bool dyn = a.sched != nullptr && kt.ntiles > nwarps * static_cast<int64_t>(CLAIM);
     int64_t cend = 0;
     const int64_t first_dyn = nwarps * CLAIM;  // first claim static, then tickets (see k_fused_ldg)
     if (dyn) {
@@ -684,8 +705,12 @@ __global__ void __launch_bounds__(WIDE ? 512 : 256, WIDE ? 1 : CDSGD_K2_MINB) k_
                 sbnd = (so0 + 1) * a.gs.chunk;
             }
             if (fast) {
-                apply_vec_tile<NR, TW>(a, s_upd, s_upd64, nr, lane, e0, w0, ne, nw, do_loc, so0, sbnd, isq, gsq2,
-                                       bad_idx);
+                if (ne == TILE_ELEMS)
+                    apply_vec_tile<NR, TW, true>(a, s_upd, s_upd64, nr, lane, e0, w0, ne, nw, do_loc, so0, sbnd, isq,
+                                                 gsq2, bad_idx);
+                else
+                    apply_vec_tile<NR, TW, false>(a, s_upd, s_upd64, nr, lane, e0, w0, ne, nw, do_loc, so0, sbnd, isq,
+                                                  gsq2, bad_idx);
             } else {
                 // generic path: lane l owns element 32s + l; word (2s + l/16), code l%16
                 uint32_t wv[MAX_RANKS];
@@ -729,17 +754,8 @@ __global__ void __launch_bounds__(WIDE ? 512 : 256, WIDE ? 1 : CDSGD_K2_MINB) k_
             }
         }
     }
-    if (a.gnorm != nullptr) {
-        gsq += static_cast<double>(isq) * tab.sq_scale;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) gsq += __shfl_xor_sync(FULL, gsq, o);
-        if (lane == 0 && gsq != 0.0) atomicAdd(a.gnorm, gsq);
-    }
-    if (a.gnorm2 != nullptr) {
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) gsq2 += __shfl_xor_sync(FULL, gsq2, o);
-        if (lane == 0 && gsq2 != 0.0) atomicAdd(a.gnorm2, gsq2);
-    }
+    if (a.gnorm != nullptr) block_atomic_add(gsq + static_cast<double>(isq) * tab.sq_scale, a.gnorm);
+    if (a.gnorm2 != nullptr) block_atomic_add(gsq2, a.gnorm2);
     if (a.err != nullptr) {
         bad_idx = warp_min_u64(bad_idx);
         if (lane == 0 && bad_idx != NO_ERR)

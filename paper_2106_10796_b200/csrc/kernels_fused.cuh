@@ -57,7 +57,12 @@ struct FusedArgs {
 // element e0 / word w0, all loads issued before any use. A key's last tile (ne < TILE_ELEMS
 // elements) uses masked accesses; padding quantizes to code 00 (the
 // reference's zero padding of the last word, codec.py:131-143) and is never stored.
-template <int NR, int APPLY, int CH, typename TW>
+// FULL: a whole tile (ne == TILE_ELEMS), every access unmasked — the compiler drops the
+// masked-access branches and their registers (CDSGD_FULL_SPEC=0 disables the split).
+#ifndef CDSGD_FULL_SPEC
+#define CDSGD_FULL_SPEC 1
+#endif
+template <int NR, int APPLY, int CH, typename TW, bool FULL>
 __device__ __forceinline__ uint32_t fused_vec_task(const FusedArgs& a, const float* s_upd, const double* s_upd64,
                                                    int lane, int64_t e0, int64_t w0, int ne, int nw, int c0,
                                                    bool a_off, bool q_off, uint32_t ahi, uint32_t alo,
@@ -76,7 +81,7 @@ __device__ __forceinline__ uint32_t fused_vec_task(const FusedArgs& a, const flo
 #pragma unroll
     for (int c = 0; c < CH; ++c) {
         const int64_t e = e0 + 128 * (c0 + c) + 4 * lane;
-        const int nv = nvalid4(ne, 128 * (c0 + c) + 4 * lane);
+        const int nv = FULL ? 4 : nvalid4(ne, 128 * (c0 + c) + 4 * lane);
         gv[c] = ld_stream_m(a.g + e, nv);
         rv[c] = ld_stream_m(a.r_in + e, nv);
         ldw4(W + e, nv, wv[c]);
@@ -87,7 +92,7 @@ __device__ __forceinline__ uint32_t fused_vec_task(const FusedArgs& a, const flo
 #pragma unroll
     for (int c = 0; c < CH; ++c) {
         const int64_t e = e0 + 128 * (c0 + c) + 4 * lane;
-        const int nv = nvalid4(ne, 128 * (c0 + c) + 4 * lane);
+        const int nv = FULL ? 4 : nvalid4(ne, 128 * (c0 + c) + 4 * lane);
         float g4[4] = {gv[c].x, gv[c].y, gv[c].z, gv[c].w};
         WV<TW>& w4 = wv[c];
         double r4[4] = {rv[c].x, rv[c].y, rv[c].z, rv[c].w};
@@ -170,8 +175,16 @@ __device__ __forceinline__ uint32_t fused_vec_task(const FusedArgs& a, const flo
 // tile issued first), two 256-thread CTAs per SM, dynamic tile scheduling.
 // CH = chunks of 128 elements per task: 4 (a whole tile) for large layouts, 1 for small
 // ones (ResNet-20-sized), where 4x more warps in flight beat the per-tile latency chain.
+// fp64 weights add 8 B per element to each task's loads in flight (g 16 + r 32 + W 32 bytes per
+// lane per chunk): CDSGD_F64_MINB / CDSGD_F64_CH select CTAs per SM and chunks per task for TW=double.
+#ifndef CDSGD_F64_MINB
+#define CDSGD_F64_MINB 2
+#endif
+#ifndef CDSGD_F64_CH
+#define CDSGD_F64_CH 4
+#endif
 template <int NR, int APPLY, int CH = CHUNKS, typename TW = float>
-__global__ void __launch_bounds__(256, 2) k_fused_ldg(FusedArgs a, KeyTab kt, DecodeTab tab) {
+__global__ void __launch_bounds__(256, sizeof(TW) == 8 ? CDSGD_F64_MINB : 2) k_fused_ldg(FusedArgs a, KeyTab kt, DecodeTab tab) {
     constexpr int SPL = CHUNKS / CH;  // tasks per tile
     __shared__ float s_upd[2 * MAX_RANKS + 1];
     __shared__ double s_upd64[2 * MAX_RANKS + 1];
@@ -204,7 +217,9 @@ __global__ void __launch_bounds__(256, 2) k_fused_ldg(FusedArgs a, KeyTab kt, De
     const int64_t nwarps = (int64_t)gridDim.x * blockDim.x / 32;
     const unsigned CLAIM = ntasks < 4 * nwarps ? 1u : 2u;
     const int64_t tail_from = ntasks - nwarps;
-    const bool dyn = a.sched != nullptr;
+    // one wave of tasks (small layouts): each warp takes its own, no ticket and no end-of-launch
+    // ticket reset (a fence + atomic per CTA on one counter)
+    const bool dyn = a.sched != nullptr && ntasks > nwarps * static_cast<int64_t>(CLAIM);
     int64_t cbase = 0, cend = 0;
     // first claim static (warp w: tasks [w*CLAIM, (w+1)*CLAIM)), later claims from the ticket
     // offset by nwarps*CLAIM: no burst of one atomic per warp on a single counter at launch
@@ -248,8 +263,12 @@ __global__ void __launch_bounds__(256, 2) k_fused_ldg(FusedArgs a, KeyTab kt, De
             if (!fast && c0 != 0) continue;  // misaligned tiles: one task does the whole tile
             uint32_t myword = 0;
             if (fast) {
-                myword = fused_vec_task<NR, APPLY, CH, TW>(a, s_upd, s_upd64, lane, e0, w0, ne, nw, c0, a_off, q_off,
-                                                           ahi, alo, bad_idx, bad_sym, gsq, isq);
+                if (CDSGD_FULL_SPEC && ne == TILE_ELEMS)
+                    myword = fused_vec_task<NR, APPLY, CH, TW, true>(a, s_upd, s_upd64, lane, e0, w0, ne, nw, c0, a_off,
+                                                                     q_off, ahi, alo, bad_idx, bad_sym, gsq, isq);
+                else
+                    myword = fused_vec_task<NR, APPLY, CH, TW, false>(a, s_upd, s_upd64, lane, e0, w0, ne, nw, c0, a_off,
+                                                                      q_off, ahi, alo, bad_idx, bad_sym, gsq, isq);
             } else {
                 uint32_t cw[APPLY == APPLY_Q ? NR : 1];
                 if constexpr (APPLY == APPLY_Q) {
@@ -328,12 +347,7 @@ __global__ void __launch_bounds__(256, 2) k_fused_ldg(FusedArgs a, KeyTab kt, De
             }
         }
     }
-    if (a.gnorm != nullptr) {
-        gsq += static_cast<double>(isq) * tab.sq_scale;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) gsq += __shfl_xor_sync(FULL, gsq, o);
-        if (lane == 0 && gsq != 0.0) atomicAdd(a.gnorm, gsq);
-    }
+    if (a.gnorm != nullptr) block_atomic_add(gsq + static_cast<double>(isq) * tab.sq_scale, a.gnorm);
     if (a.err != nullptr) {
         bad_idx = warp_min_u64(bad_idx);
         bad_sym = warp_min_u64(bad_sym);

@@ -77,6 +77,31 @@ def run_case(case, exchange, comm, rank, world, dev):
     wk.close()
 
 
+def run_records_case(exchange, comm, rank, world, dev):
+    """World 2: per-round records (records.Recorder) vs the reference's own metrics.csv
+    (tests/golden/metrics_n2.csv, unmodified reference: make_metrics_golden.py)."""
+    from paper_2106_10796_b200.records import Recorder, read_metrics_csv
+
+    sizes, seed, k, warm, iters = [640, 7, 33], 4, 3, 1, 11
+    layout = Layout.from_lengths(sizes)
+    n = layout.total
+    hp = HyperParams(algo="cdsgd", workers=world, eta_global=0.1, eta_local=0.4, k=k, alpha=0.5, warmup_n=warm)
+    wk = CDSGDWorker(layout, hp, O.synthetic_weights(seed, n), rank=rank, comm=comm, exchange=exchange)
+    rec = Recorder(wk, batches_per_epoch=1)
+    for t in range(iters):
+        wk.step(torch.from_numpy(O.synthetic_grad(seed, t, rank, n)).to(dev))
+        rec.record(0.0)
+    wk.flush()
+    mine = rec.records()
+    gold = read_metrics_csv(os.path.join(ROOT, "tests", "golden", "metrics_n2.csv"))
+    assert len(mine) == len(gold) == iters
+    for g, m in zip(gold, mine):
+        assert (g.iteration, g.epoch, g.train_loss, g.bytes_pushed, g.compressed) == \
+               (m.iteration, m.epoch, m.train_loss, m.bytes_pushed, m.compressed), (g, m)
+        assert abs(g.grad_norm - m.grad_norm) <= 1e-6 * g.grad_norm, (exchange, g, m)
+    wk.close()
+
+
 def run_failure_case(exchange, comm, rank, world, dev):
     """Rank world-1 hits a non-finite gradient at round 2 (a compressed round): it raises
     CodecNumericError(round 2) with its residual rolled back, every other rank raises
@@ -116,6 +141,8 @@ def main():
     for exchange in exchanges:
         for case in CASES:
             run_case(case, exchange, comm, rank, world, dev)
+        if world == 2:
+            run_records_case(exchange, comm, rank, world, dev)
         if exchange in ("p2p", "p2p-exact"):
             run_failure_case(exchange, comm, rank, world, dev)
     comm.close()
