@@ -48,6 +48,9 @@ def parse():
     ap.add_argument("--alpha", type=float, default=0.5)
     ap.add_argument("--weights", choices=("f64", "f32"), default="f64",
                     help="global weights W: f64 = exact (the reference's fp64 W, bitwise at N=1), f32 = fast")
+    ap.add_argument("--residual", choices=("f64", "f32"), default="f64",
+                    help="error-feedback residual: f64 = exact (bitwise the reference), f32 = fast mode "
+                         "(fp32 restatement; needs --weights f32)")
     ap.add_argument("--exchange", choices=("p2p", "p2p-exact", "nccl"), default="p2p",
                     help="p2p: code all-gather fused into K1 over NVLink (symmetric memory), correction by "
                          "ncclAllReduce; p2p-exact: corrections by the exact sharded NVLink reduce too; "
@@ -337,6 +340,50 @@ def small_layout_cold(args, dev, name="resnet20", n_sets=48, rounds=8):
                    f"state+inputs > 126 MB L2): each step starts from cold L2"}
 
 
+def fast_mode_rate(args, dev, layout, steps, warmup=8):
+    """The opt-in FAST mode on the same workload at N=1: fp32 residual (the fp32 restatement
+    of the quantizer, 12.25 instead of 20.25 B/elem) and fp32 weights. Not the reference's
+    arithmetic (the headline is the exact mode); reported beside it as SURVEY §8(b)/(c) ask."""
+    import torch
+
+    from paper_2106_10796_b200.engine import HyperParams
+    from paper_2106_10796_b200.worker import CDSGDWorker
+
+    n = layout.total
+    hp = HyperParams(algo="cdsgd", workers=1, eta_global=0.1, eta_local=0.4, k=args.k, alpha=args.alpha, warmup_n=0)
+    gen = torch.Generator(device=dev).manual_seed(77)
+    pool = [0.3 * torch.randn(n, device=dev, generator=gen) for _ in range(2)]
+    wk = CDSGDWorker(layout, hp, torch.zeros(n, device=dev), weights="f32", residual="f32")
+    for i in range(warmup):
+        wk.step(pool[i % 2])
+    torch.cuda.synchronize(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for i in range(steps):
+        wk.step(pool[i % 2])
+    e1.record()
+    e1.synchronize()
+    ms = e0.elapsed_time(e1)
+    wk.profile_begin()
+    for i in range(steps):
+        wk.step(pool[i % 2])
+    prof = wk.profile_end()
+    wk.check()
+    wk.close()
+    nw = layout.n_words
+    peak, _ = hbm_peak()
+    fb = 4 * n + 8 * n + 8 * n + 4 * n + 4 * nw + 4 * nw  # g | r r/w (fp32) | W r/w (fp32) | loc | codes in+out
+    f = prof["fused"]
+    out = {"residual": "fp32 (FAST mode: bitwise the fp32 restatement oracle, not the reference)",
+           "weights": "fp32", "value": n * steps / (ms / 1e3) / 1e9, "unit": UNIT, "ms_per_step": ms / steps,
+           "steps": steps}
+    if f["n"]:
+        us = 1e3 * f["ms"] / f["n"]
+        out["fused"] = {"avg_us": us, "bytes_per_elem": fb / n, "achieved_gbs": fb / us / 1e3,
+                        "frac": fb / us / 1e3 / peak}
+    return out
+
+
 def allreduce_standalone(comm, n, dev, reps=20):
     """Bus bandwidth of the correction all-reduce ALONE (nothing else on the GPU): the same
     ncclAllReduce(fp32 sum) of n elements on the engine's communicator (nccl-tests bus bytes
@@ -411,10 +458,21 @@ def self_check(wk, layout, pools, seq, w0, world, rank, dev, args, keys=(0, None
         else:
             sizes = [b - a for a, b in sl]
             w0s = np.concatenate([w0[a:b] for a, b in sl]).astype(np.float64)
-            port = cpu_port.CPortEngine(w0s, sizes, world, k=args.k, alpha=args.alpha, eta_g=0.1, eta_l=0.4)
-            for p in seq:
-                port.step(got["g0"] if p == 0 else got["g1"])
-            res_ok = all(np.array_equal(got["res"][r].view(np.uint64), port.res[r].view(np.uint64))
+            if args.residual == "f32":  # fast mode: the fp32 restatement (NumPy lock-step oracle)
+                from oracle import cdsgd_oracle as O
+
+                port = O.LockstepOracle(w0s, sizes, O.OracleHP("cdsgd", world, 0.1, 0.4, args.k, args.alpha, 0),
+                                        residual="f32")
+                for p in seq:
+                    port.step(list(got["g0"] if p == 0 else got["g1"]))
+                port.res = [ow.residual for ow in port.workers]
+                port.loc = [port.compute_weights(r) for r in range(world)]
+            else:
+                port = cpu_port.CPortEngine(w0s, sizes, world, k=args.k, alpha=args.alpha, eta_g=0.1, eta_l=0.4)
+                for p in seq:
+                    port.step(got["g0"] if p == 0 else got["g1"])
+            vt = np.uint32 if args.residual == "f32" else np.uint64
+            res_ok = all(np.array_equal(got["res"][r].view(vt), np.asarray(port.res[r]).view(vt))
                          for r in range(world))
             dW = np.abs(got["W"][0].astype(np.float64) - port.W)
             dl = max(float(np.abs(got["loc"][r].astype(np.float64) - port.loc[r]).max()) for r in range(world))
@@ -464,7 +522,7 @@ def run_ours(args):
     w0 = torch.randn(n, device=dev, generator=torch.Generator(device=dev).manual_seed(999))
     pool = [0.3 * torch.randn(n, device=dev, generator=gen) for _ in range(2)]
     wk = CDSGDWorker(layout, hp, w0, rank=rank, comm=comm, gnorm_ring=64, exchange=args.exchange,
-                     weights=args.weights)
+                     weights=args.weights, residual=args.residual)
     stream = torch.cuda.current_stream(dev)
 
     def barrier():
@@ -524,17 +582,18 @@ def run_ours(args):
     # ---------------- per-kernel roofline (algorithmic bytes / avg CUDA-event duration)
     peak, peak_src = hbm_peak()
     wb = 8 if args.weights == "f64" else 4  # bytes per global weight
+    rb = 8 if args.residual == "f64" else 4  # bytes per residual element
     alg = {
-        "quantize": 4 * n + 8 * n + 8 * n + 4 * nw,
+        "quantize": 4 * n + 2 * rb * n + 4 * nw,
         # W r/w | g_next 4 | loc 4 | codes N/4
         "apply_quant": 2 * wb * n + 4 * n + 4 * n + world * 4 * nw,
         # W r/w | gsum 4 | g_next 4 | loc 4
         "apply_full": 2 * wb * n + 3 * 4 * n,
         "local_update": wb * n + 2 * 4 * n,
         # apply(t-1) + quantize(t): g 4 | r 8+8 | W r/w | loc 4 | codes in N/4 + out 1/4
-        "fused": 4 * n + 16 * n + 2 * wb * n + 4 * n + world * 4 * nw + 4 * nw,
+        "fused": 4 * n + 2 * rb * n + 2 * wb * n + 4 * n + world * 4 * nw + 4 * nw,
         # quantize(t) + loc_{t+1} = W_t - eta_l*g_t (nothing to apply): g 4 | r 8+8 | W read | loc 4 | codes 1/4
-        "fused_local": 4 * n + 16 * n + wb * n + 4 * n + 4 * nw,
+        "fused_local": 4 * n + 2 * rb * n + wb * n + 4 * n + 4 * nw,
         # P2P correction: stage g (4+4); reduce of my shard n/N: N stage reads + W r/w (+ N-1 remote W writes)
         "stage": 8 * n,
         "reduce": (world * 4 * n + wb * n + world * wb * n) // max(world, 1),
@@ -650,6 +709,8 @@ def run_ours(args):
     if world == 1 and args.workload == "resnet50" and not args.no_secondary:
         secondary = {"resnet20": small_layout_rate(args, dev)}
         secondary["resnet20"]["cold_l2"] = small_layout_cold(args, dev)
+        if args.residual == "f64":
+            secondary["fast_mode"] = fast_mode_rate(args, dev, layout, K)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -662,7 +723,9 @@ def run_ours(args):
             "dtype": "f64", "data": "synthetic",
             "config": {"workload": workload_desc(layout, args.workload), "layout": args.workload,
                        "n_per_rank": n, "keys": len(layout), "k": args.k, "alpha": args.alpha, "algo": "cdsgd",
-                       "warmup_n": 0, "residual": "fp64 (bit-exact)",
+                       "warmup_n": 0,
+                       "residual": ("fp64 (bit-exact)" if args.residual == "f64"
+                                    else "fp32 (FAST mode: bitwise the fp32 restatement, not the reference)"),
                        "weights": ("fp64 (exact: the reference's W bit for bit at N=1)" if args.weights == "f64"
                                    else "fp32 (fast: one fp32 rounding per round)"),
                        "exchange": exchange_desc(args.exchange, world),

@@ -93,6 +93,13 @@ int cdsgd_quantize(const cdsgd_layout* layout, const void* grad, int32_t grad_dt
                    const double* r_in, double* r_out, uint32_t* words, double alpha,
                    uint64_t* err, uint64_t err_tag, void* stream);
 
+/* FAST MODE (opt-in, not the reference's arithmetic): cdsgd_quantize restated in fp32 —
+ * acc = r_in + g, +a if acc >= a, -a if acc <= -a (a = (float)alpha), r_out = acc - emitted,
+ * all fp32 — for an fp32 residual: 12.25 instead of 20.25 bytes per element. Bitwise against
+ * the fp32 restatement oracle (oracle/cdsgd_oracle.py quantize_f32), not the reference. */
+int cdsgd_quantize_f32r(const cdsgd_layout* layout, const float* grad, const float* r_in, float* r_out,
+                        uint32_t* words, double alpha, uint64_t* err, uint64_t err_tag, void* stream);
+
 /* Replaces codec.dequantize (codec.py:197-206) when n_payloads == 1 and the
  * quantized branch of engine.server_aggregate (engine.py:249-255) otherwise:
  * out[i] = (sum over payload p ascending of decode_p[i]) / n_payloads, fp64.
@@ -147,8 +154,8 @@ int cdsgd_apply_full(void* weights, int32_t w_dtype, const float* gsum, int32_t 
  * The apply part is skipped if *err < skip_below. nranks <= 8. Decode as K2 (exact table
  * when every j*alpha is representable, else the sequential fp64 sum). gnorm_sq: += the
  * round t-1 mean's sum of squares (nullable). */
-int cdsgd_fused_round(const cdsgd_layout* layout, const float* grad, const double* r_in, double* r_out,
-                      uint32_t* words, double alpha, uint64_t* err, uint64_t err_tag, void* weights,
+int cdsgd_fused_round(const cdsgd_layout* layout, const float* grad, const void* r_in, void* r_out,
+                      int32_t r_dtype, uint32_t* words, double alpha, uint64_t* err, uint64_t err_tag, void* weights,
                       int32_t w_dtype, float* loc, const uint32_t* gathered, int32_t nranks, int64_t rank_stride_words,
                       double eta_g, double eta_l, uint64_t skip_below, double* gnorm_sq, void* stream);
 
@@ -196,10 +203,12 @@ typedef struct {
     int32_t gnorm_ring;     /* entries in gnorm_sq (0 = no grad-norm metric) */
     int32_t weights_dtype;  /* CDSGD_F64: exact (the reference's fp64 W, bitwise on compressed rounds);
                                CDSGD_F32: fast (W rounded to fp32 every round) */
+    int32_t residual_dtype; /* CDSGD_F64: exact (bitwise the reference's residual and codes);
+                               CDSGD_F32: fast mode (fp32 restatement, 12.25 B/elem quantizer; needs fp32 W) */
     double alpha, eta_global, eta_local;
     void* weights;           /* [n] fp64 or fp32 (weights_dtype), replicated global weights W */
     float* loc;              /* [n] fp32, local (compute) weights */
-    double* residual[2];     /* [n] fp64 each, ping-pong error-feedback residual */
+    void* residual[2];       /* [n] fp64 (or fp32: residual_dtype) each, ping-pong error-feedback residual */
     uint32_t* gathered[2];   /* [nranks * words] each */
     float* gsum[2];          /* [n] fp32 each (nranks > 1; may be NULL when nranks == 1) */
     uint64_t* err;           /* [2] device words, init CDSGD_NO_ERROR */

@@ -122,6 +122,50 @@ def quantize(residual: np.ndarray, grad: np.ndarray, alpha: float):
     return pack_symbols(sym), acc - emitted                      # codec.py:192-193
 
 
+def quantize_f32(residual: np.ndarray, grad: np.ndarray, alpha: float):
+    """FAST-MODE restatement of codec.py:181-193 in float32 (NOT the reference's arithmetic,
+    which is fp64): the same operations in the same order with fp32 operands and threshold
+    a = float32(alpha) — acc = r + g; plus = acc >= a; minus = acc <= -a; emitted =
+    where(plus, a, 0) + where(minus, -a, 0); r' = acc - emitted. Pins the GPU's fp32-residual
+    mode (cdsgd_quantize_f32r) bitwise; same error semantics as quantize()."""
+    if alpha <= 0:
+        raise ValueError("threshold alpha must be > 0")
+    a = np.float32(alpha)
+    g = np.asarray(grad, dtype=np.float32)
+    r = np.asarray(residual, dtype=np.float32)
+    if g.shape != r.shape:
+        raise ValueError("gradient length does not match residual")
+    acc = r + g                                                  # codec.py:181, fp32
+    finite = np.isfinite(acc)
+    if not finite.all():                                         # codec.py:182-185
+        bad = int(np.argmin(finite))
+        raise OracleNumericError(f"non-finite accumulated gradient at element {bad}", bad)
+    plus = acc >= a                                              # codec.py:186
+    minus = acc <= -a                                            # codec.py:187
+    sym = np.zeros(acc.shape[0], dtype=np.uint8)
+    sym[plus] = SYM_PLUS
+    sym[minus] = SYM_MINUS
+    emitted = np.where(plus, a, np.float32(0)) + np.where(minus, -a, np.float32(0))  # codec.py:191, fp32
+    return pack_symbols(sym), (acc - emitted).astype(np.float32)  # codec.py:192-193
+
+
+def quantize_layout_f32(residual, grad, alpha, sizes):
+    """quantize_layout with the fp32 restatement (fast mode)."""
+    eoff, woff = layout_offsets(sizes)
+    words = np.zeros(int(woff[-1]), dtype=np.uint32)
+    r_new = np.empty(int(eoff[-1]), dtype=np.float32)
+    for k in range(len(sizes)):
+        sl = slice(int(eoff[k]), int(eoff[k + 1]))
+        try:
+            w, r = quantize_f32(residual[sl], grad[sl], alpha)
+        except OracleNumericError as exc:
+            exc.key = k
+            raise
+        words[int(woff[k]) : int(woff[k + 1])] = w
+        r_new[sl] = r
+    return words, r_new
+
+
 def dequantize(words: np.ndarray, threshold: float, length: int) -> np.ndarray:
     """Decode to {-t, 0, +t} float64; reserved 11 -> error at first index — codec.py:197-206."""
     sym = unpack_symbols(words, length)
@@ -284,8 +328,10 @@ class LockstepOracle:
     reference line for line, in float64.
     """
 
-    def __init__(self, w0: np.ndarray, sizes, hp: OracleHP):
+    def __init__(self, w0: np.ndarray, sizes, hp: OracleHP, residual: str = "f64"):
+        """residual="f32": the fast-mode restatement (quantize_f32); everything else fp64."""
         self.hp = hp
+        self.residual_dtype = residual
         self.sizes = [int(s) for s in sizes]
         self.n = int(sum(self.sizes))
         self.W = np.asarray(w0, dtype=np.float64).copy()          # ServerNode.weights, engine.py:448
@@ -294,7 +340,8 @@ class LockstepOracle:
         self.n_warmup = hp.warmup_n if hp.algo in ("lusgd", "cdsgd") else 0       # engine.py:314
         self.workers = []
         for w in range(hp.workers):
-            ow = _OWorker(w, 0, self.W.copy(), [None, None], np.zeros(self.n))
+            ow = _OWorker(w, 0, self.W.copy(), [None, None],
+                          np.zeros(self.n, dtype=np.float32 if residual == "f32" else np.float64))
             if self.uses_local and self.n_warmup == 0:           # engine.py:318-322
                 ow.slots = [self.W.copy(), self.W.copy()]
             self.workers.append(ow)
@@ -348,7 +395,11 @@ class LockstepOracle:
             compressed = self._push_compressed(ow)               # engine.py:394
             flags.add(compressed)
             if compressed:                                        # engine.py:397-404
-                words, ow.residual = quantize_layout(ow.residual, g64, hp.alpha, self.sizes)
+                if self.residual_dtype == "f32":
+                    words, ow.residual = quantize_layout_f32(ow.residual, np.asarray(g, np.float32), hp.alpha,
+                                                             self.sizes)
+                else:
+                    words, ow.residual = quantize_layout(ow.residual, g64, hp.alpha, self.sizes)
                 self.words[(t, ow.wid)] = words
                 contrib.append(dequantize_layout(words, hp.alpha, self.sizes))
             else:

@@ -23,6 +23,7 @@ ALGO = {"ssgd": 0, "lusgd": 1, "bitsgd": 2, "cdsgd": 3}
 UNIQUE_ID_BYTES = 128
 ABI_VERSION = 2
 WEIGHTS = {"f64": 1, "f32": 0}  # CDSGD_F64 (exact, default) / CDSGD_F32 (fast)
+RESIDUAL = WEIGHTS  # residual_dtype: f64 exact (default) / f32 fast mode (needs fp32 weights)
 
 vp = C.c_void_p
 i32 = C.c_int32
@@ -35,6 +36,7 @@ class EngineDesc(C.Structure):
     _fields_ = [
         ("algo", i32), ("nranks", i32), ("rank", i32), ("k", i32), ("warmup_n", i32),
         ("force_compress", i32), ("bypass_local", i32), ("gnorm_ring", i32), ("weights_dtype", i32),
+        ("residual_dtype", i32),
         ("alpha", f64), ("eta_global", f64), ("eta_local", f64),
         ("weights", vp), ("loc", vp), ("residual", vp * 2), ("gathered", vp * 2), ("gsum", vp * 2),
         ("err", vp), ("gnorm_sq", vp),
@@ -68,7 +70,9 @@ _SIGS = {
     "cdsgd_local_update": (C.c_int, [vp, i32, vp, i32, vp, i32, i64, f64, vp]),
     "cdsgd_apply_quant": (C.c_int, [vp, vp, i32, vp, i32, i64, f64, f64, vp, vp, f64, vp, u64, vp, vp]),
     "cdsgd_apply_full": (C.c_int, [vp, i32, vp, i32, i64, f64, vp, vp, f64, vp, u64, vp, vp]),
-    "cdsgd_fused_round": (C.c_int, [vp, vp, vp, vp, vp, f64, vp, u64, vp, i32, vp, vp, i32, i64, f64, f64, u64, vp, vp]),
+    "cdsgd_fused_round": (C.c_int, [vp, vp, vp, vp, i32, vp, f64, vp, u64, vp, i32, vp, vp, i32, i64, f64, f64, u64, vp,
+                                    vp]),
+    "cdsgd_quantize_f32r": (C.c_int, [vp, vp, vp, vp, vp, f64, vp, u64, vp]),
     "cdsgd_comm_unique_id": (C.c_int, [vp]),
     "cdsgd_comm_init": (C.c_int, [vp, i32, i32, C.POINTER(vp)]),
     "cdsgd_comm_destroy": (C.c_int, [vp]),

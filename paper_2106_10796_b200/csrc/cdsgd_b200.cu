@@ -202,16 +202,24 @@ int launch_af_tma_cfg(const ApplyFArgs& a, int wdt, cudaStream_t st) {
         default: return launch_af_tma<8, 4>(a, st);
     }
 }
-template <typename G, int WARPS, int ST>
-int launch_quant_tma(const G* g, const double* r_in, double* r_out, uint32_t* words, KeyTab kt, double alpha,
+template <typename G, int WARPS, int ST, typename TR = double>
+int launch_quant_tma(const G* g, const TR* r_in, TR* r_out, uint32_t* words, KeyTab kt, double alpha,
                      uint64_t* err, uint64_t tag, cudaStream_t st, const P2PArgs& x) {
-    using SM = QuantSmem<G, WARPS, ST>;
+    using SM = QuantSmem<G, WARPS, ST, TR>;
     static_assert(SM::BYTES <= 227 * 1024, "smem");
-    if (!prepare_tma(k_quantize_tma<G, WARPS, ST>, SM::BYTES)) return fail(CDSGD_ERR_CUDA, "smem attribute");
-    launch_pdl(k_quantize_tma<G, WARPS, ST>, tma_grid(kt.ntiles, WARPS), WARPS * 32, SM::BYTES, st, g, r_in, r_out,
+    if (!prepare_tma(k_quantize_tma<G, WARPS, ST, TR>, SM::BYTES)) return fail(CDSGD_ERR_CUDA, "smem attribute");
+    launch_pdl(k_quantize_tma<G, WARPS, ST, TR>, tma_grid(kt.ntiles, WARPS), WARPS * 32, SM::BYTES, st, g, r_in, r_out,
                words, kt, alpha, err, tag, x);
     return CDSGD_OK;
 }
+// fp32-residual fast mode: 16 warps x 3 stages of 4 KB slots (g + r, fp32)
+int launch_quant_tma_cfg(const float* g, const float* r_in, float* r_out, uint32_t* words, KeyTab kt, double alpha,
+                         uint64_t* err, uint64_t tag, cudaStream_t st, const P2PArgs& x) {
+    return launch_quant_tma<float, 16, 3, float>(g, r_in, r_out, words, kt, alpha, err, tag, st, x);
+}
+// residual of either type behind void* (the engine's residual_dtype)
+int launch_quant_tma_rdt(const float* g, int rdt, const void* r_in, void* r_out, uint32_t* words, KeyTab kt,
+                         double alpha, uint64_t* err, uint64_t tag, cudaStream_t st, const P2PArgs& x);
 template <typename G>
 int launch_quant_tma_cfg(const G* g, const double* r_in, double* r_out, uint32_t* words, KeyTab kt, double alpha,
                          uint64_t* err, uint64_t tag, cudaStream_t st, const P2PArgs& x) {
@@ -226,6 +234,14 @@ int launch_quant_tma_cfg(const G* g, const double* r_in, double* r_out, uint32_t
         default: return launch_quant_tma<G, 16, 2>(g, r_in, r_out, words, kt, alpha, err, tag, st, x);
     }
     }
+}
+int launch_quant_tma_rdt(const float* g, int rdt, const void* r_in, void* r_out, uint32_t* words, KeyTab kt,
+                         double alpha, uint64_t* err, uint64_t tag, cudaStream_t st, const P2PArgs& x) {
+    if (rdt == CDSGD_F32)
+        return launch_quant_tma_cfg(g, static_cast<const float*>(r_in), static_cast<float*>(r_out), words, kt, alpha,
+                                    err, tag, st, x);
+    return launch_quant_tma_cfg(g, static_cast<const double*>(r_in), static_cast<double*>(r_out), words, kt, alpha,
+                                err, tag, st, x);
 }
 }  // namespace
 
@@ -324,6 +340,19 @@ extern "C" int cdsgd_quantize(const cdsgd_layout* L, const void* grad, int32_t g
                                   S(stream), nox);
     else
         return fail(CDSGD_ERR_ARG, "grad dtype must be CDSGD_F32 or CDSGD_F64");
+    if (rc != CDSGD_OK) return rc;
+    LAUNCH_CHECK();
+    return CDSGD_OK;
+}
+
+extern "C" int cdsgd_quantize_f32r(const cdsgd_layout* L, const float* grad, const float* r_in, float* r_out,
+                                   uint32_t* words, double alpha, uint64_t* err, uint64_t tag, void* stream) {
+    if (L == nullptr) return fail(CDSGD_ERR_ARG, "layout is NULL");
+    if (!(alpha > 0.0)) return fail(CDSGD_ERR_ARG, "threshold alpha must be > 0");
+    if (L->n == 0) return CDSGD_OK;
+    if (!grad || !r_in || !r_out || !words) return fail(CDSGD_ERR_ARG, "NULL buffer");
+    const P2PArgs nox{};
+    const int rc = launch_quant_tma_cfg(grad, r_in, r_out, words, L->tab(), alpha, err, tag, S(stream), nox);
     if (rc != CDSGD_OK) return rc;
     LAUNCH_CHECK();
     return CDSGD_OK;
@@ -557,40 +586,44 @@ int launch_apply_full(void* W, int wdt, const float* gsum, int nr, int64_t n, do
     return CDSGD_OK;
 }
 // Fused apply(t-1) + quantize(t), register-staged (measured faster than a TMA-ring variant).
-template <int NR, int AP, typename TW>
+template <int NR, int AP, typename TW, typename TR>
 int launch_fused_cfg(const FusedArgs& a, const KeyTab& kt, const DecodeTab& tab, cudaStream_t st) {
     constexpr int CHL = sizeof(TW) == 8 ? CDSGD_F64_CH : CHUNKS;  // chunks per task on large layouts
     // fewer than 2 whole-tile tasks per resident warp: split tiles into chunk tasks
     const int64_t warps =
-        static_cast<int64_t>(resident_blocks(k_fused_ldg<NR, AP, CHL, TW>, THREADS)) * WARPS_PER_BLOCK;
+        static_cast<int64_t>(resident_blocks(k_fused_ldg<NR, AP, CHL, TW, TR>, THREADS)) * WARPS_PER_BLOCK;
     if (kt.ntiles < 2 * warps)
-        launch_pdl(k_fused_ldg<NR, AP, 1, TW>, tile_grid(k_fused_ldg<NR, AP, 1, TW>, kt.ntiles * CHUNKS), THREADS, 0, st,
-                   a, kt, tab);
+        launch_pdl(k_fused_ldg<NR, AP, 1, TW, TR>, tile_grid(k_fused_ldg<NR, AP, 1, TW, TR>, kt.ntiles * CHUNKS), THREADS,
+                   0, st, a, kt, tab);
     else
-        launch_pdl(k_fused_ldg<NR, AP, CHL, TW>, tile_grid(k_fused_ldg<NR, AP, CHL, TW>, kt.ntiles * (CHUNKS / CHL)),
-                   THREADS, 0, st, a, kt, tab);
+        launch_pdl(k_fused_ldg<NR, AP, CHL, TW, TR>,
+                   tile_grid(k_fused_ldg<NR, AP, CHL, TW, TR>, kt.ntiles * (CHUNKS / CHL)), THREADS, 0, st, a, kt, tab);
     return CDSGD_OK;
 }
-template <typename TW>
+template <typename TW, typename TR>
 int launch_fused_t(int nr, int apply, const FusedArgs& a, const KeyTab& kt, const DecodeTab& tab, cudaStream_t st) {
-    if (apply == APPLY_L) return launch_fused_cfg<1, APPLY_L, TW>(a, kt, tab, st);  // W final: loc + quantize only
-    if (apply == APPLY_F) return launch_fused_cfg<1, APPLY_F, TW>(a, kt, tab, st);
+    if (apply == APPLY_L) return launch_fused_cfg<1, APPLY_L, TW, TR>(a, kt, tab, st);  // W final: loc + quantize only
+    if (apply == APPLY_F) return launch_fused_cfg<1, APPLY_F, TW, TR>(a, kt, tab, st);
     switch (nr) {
-        case 1: return launch_fused_cfg<1, APPLY_Q, TW>(a, kt, tab, st);
-        case 2: return launch_fused_cfg<2, APPLY_Q, TW>(a, kt, tab, st);
-        case 3: return launch_fused_cfg<3, APPLY_Q, TW>(a, kt, tab, st);
-        case 4: return launch_fused_cfg<4, APPLY_Q, TW>(a, kt, tab, st);
-        case 5: return launch_fused_cfg<5, APPLY_Q, TW>(a, kt, tab, st);
-        case 6: return launch_fused_cfg<6, APPLY_Q, TW>(a, kt, tab, st);
-        case 7: return launch_fused_cfg<7, APPLY_Q, TW>(a, kt, tab, st);
-        case 8: return launch_fused_cfg<8, APPLY_Q, TW>(a, kt, tab, st);
+        case 1: return launch_fused_cfg<1, APPLY_Q, TW, TR>(a, kt, tab, st);
+        case 2: return launch_fused_cfg<2, APPLY_Q, TW, TR>(a, kt, tab, st);
+        case 3: return launch_fused_cfg<3, APPLY_Q, TW, TR>(a, kt, tab, st);
+        case 4: return launch_fused_cfg<4, APPLY_Q, TW, TR>(a, kt, tab, st);
+        case 5: return launch_fused_cfg<5, APPLY_Q, TW, TR>(a, kt, tab, st);
+        case 6: return launch_fused_cfg<6, APPLY_Q, TW, TR>(a, kt, tab, st);
+        case 7: return launch_fused_cfg<7, APPLY_Q, TW, TR>(a, kt, tab, st);
+        case 8: return launch_fused_cfg<8, APPLY_Q, TW, TR>(a, kt, tab, st);
         default: return fail(CDSGD_ERR_ARG, "fused step supports 1..8 ranks");
     }
 }
-int launch_fused(int nr, int apply, int wdt, const FusedArgs& a, const KeyTab& kt, const DecodeTab& tab,
+// weight / residual precision modes: exact (fp64 W, fp64 r), fp32 W (fp64 r), fast (fp32 W, fp32 r)
+bool modes_ok(int wdt, int rdt) { return rdt == CDSGD_F64 ? (wdt == CDSGD_F64 || wdt == CDSGD_F32) : wdt == CDSGD_F32; }
+int launch_fused(int nr, int apply, int wdt, int rdt, const FusedArgs& a, const KeyTab& kt, const DecodeTab& tab,
                  cudaStream_t st) {
-    const int rc = wdt == CDSGD_F64 ? launch_fused_t<double>(nr, apply, a, kt, tab, st)
-                                    : launch_fused_t<float>(nr, apply, a, kt, tab, st);
+    if (!modes_ok(wdt, rdt)) return fail(CDSGD_ERR_ARG, "fp32 residuals need fp32 weights (the fast mode)");
+    const int rc = rdt == CDSGD_F32   ? launch_fused_t<float, float>(nr, apply, a, kt, tab, st)
+                   : wdt == CDSGD_F64 ? launch_fused_t<double, double>(nr, apply, a, kt, tab, st)
+                                      : launch_fused_t<float, double>(nr, apply, a, kt, tab, st);
     if (rc != CDSGD_OK) return rc;
     LAUNCH_CHECK();
     return CDSGD_OK;
@@ -614,8 +647,8 @@ extern "C" int cdsgd_apply_full(void* W, int32_t wdt, const float* gsum, int32_t
     return launch_apply_full(W, wdt, gsum, nr, n, eta_g, gnext, loc, eta_l, err, skip_below, gnorm, S(stream));
 }
 
-extern "C" int cdsgd_fused_round(const cdsgd_layout* L, const float* grad, const double* r_in, double* r_out,
-                                 uint32_t* words, double alpha, uint64_t* err, uint64_t err_tag, void* W,
+extern "C" int cdsgd_fused_round(const cdsgd_layout* L, const float* grad, const void* r_in, void* r_out,
+                                 int32_t r_dtype, uint32_t* words, double alpha, uint64_t* err, uint64_t err_tag, void* W,
                                  int32_t wdt, float* loc, const uint32_t* gathered, int32_t nr, int64_t stride, double eta_g,
                                  double eta_l, uint64_t skip_below, double* gnorm, void* stream) {
     if (L == nullptr) return fail(CDSGD_ERR_ARG, "layout is NULL");
@@ -650,7 +683,7 @@ extern "C" int cdsgd_fused_round(const cdsgd_layout* L, const float* grad, const
     a.sched = nullptr;  // static tile ranges: no scheduler state shared between callers
     DecodeTab tab;
     build_tab(tab, alpha, eta_g, nr);
-    return launch_fused(nr, gathered != nullptr ? APPLY_Q : APPLY_L, wdt, a, L->tab(), tab, S(stream));
+    return launch_fused(nr, gathered != nullptr ? APPLY_Q : APPLY_L, wdt, r_dtype, a, L->tab(), tab, S(stream));
 }
 
 // ------------------------------------------------------------------ NCCL exchange
@@ -1133,6 +1166,8 @@ extern "C" int cdsgd_engine_create(const cdsgd_engine_desc* d, const cdsgd_layou
     if (!(d->alpha > 0.0)) return fail(CDSGD_ERR_ARG, "alpha must be > 0");
     if (!(d->eta_global > 0.0) || !(d->eta_local > 0.0)) return fail(CDSGD_ERR_ARG, "learning rates must be > 0");
     if (!wdt_ok(d->weights_dtype)) return fail(CDSGD_ERR_ARG, "weights_dtype must be CDSGD_F32 or CDSGD_F64");
+    if (!wdt_ok(d->residual_dtype) || !modes_ok(d->weights_dtype, d->residual_dtype))
+        return fail(CDSGD_ERR_ARG, "residual_dtype must be CDSGD_F64, or CDSGD_F32 with fp32 weights (fast mode)");
     if (!d->weights || !d->loc || !d->residual[0] || !d->residual[1] || !d->gathered[0] || !d->gathered[1] || !d->err)
         return fail(CDSGD_ERR_ARG, "NULL engine buffer");
     if (d->nranks > 1 && (comm == nullptr || !d->gsum[0] || !d->gsum[1]))
@@ -1397,8 +1432,8 @@ extern "C" int cdsgd_engine_step(cdsgd_engine* E, const float* g, void* stream) 
             x.err = E->d.err;
             const uint64_t tag = static_cast<uint64_t>(t - E->err_base) << CDSGD_INDEX_BITS;
             const long pi = prof_start(E, 0, C);
-            rc = launch_quant_tma_cfg(g, E->d.residual[E->rcur], E->d.residual[E->rcur ^ 1], mine, E->L->tab(),
-                                      E->d.alpha, E->d.err, tag, C, x);
+            rc = launch_quant_tma_rdt(g, E->d.residual_dtype, E->d.residual[E->rcur], E->d.residual[E->rcur ^ 1], mine,
+                                      E->L->tab(), E->d.alpha, E->d.err, tag, C, x);
             if (rc == CDSGD_OK) {
                 g_launches.fetch_add(1, std::memory_order_relaxed);
                 const cudaError_t le = cudaGetLastError();
@@ -1491,7 +1526,7 @@ extern "C" int cdsgd_engine_step(cdsgd_engine* E, const float* g, void* stream) 
         E->rlog.push_back(static_cast<int8_t>(E->rcur));
         const long pi = prof_start(E, has_pend ? 5 : 9, C);
         const int ap = !has_pend ? APPLY_L : (E->pend_comp ? APPLY_Q : APPLY_F);
-        rc = launch_fused(nr, ap, E->d.weights_dtype, a, E->L->tab(), E->tab, C);
+        rc = launch_fused(nr, ap, E->d.weights_dtype, E->d.residual_dtype, a, E->L->tab(), E->tab, C);
         prof_stop(E, pi, C);
         if (rc != CDSGD_OK) return rc;
         E->rcur ^= 1;
@@ -1528,8 +1563,8 @@ extern "C" int cdsgd_engine_step(cdsgd_engine* E, const float* g, void* stream) 
             x.sc_fence = E->sc_fence;
             if (E->diag_no_wait) x.wait_value = 0;
             x.err = E->d.err;
-            rc = launch_quant_tma_cfg(g, E->d.residual[E->rcur], E->d.residual[E->rcur ^ 1], mine, E->L->tab(),
-                                      E->d.alpha, E->d.err, tag, C, x);
+            rc = launch_quant_tma_rdt(g, E->d.residual_dtype, E->d.residual[E->rcur], E->d.residual[E->rcur ^ 1], mine,
+                                      E->L->tab(), E->d.alpha, E->d.err, tag, C, x);
             if (rc == CDSGD_OK) {
                 g_launches.fetch_add(1, std::memory_order_relaxed);
                 const cudaError_t le = cudaGetLastError();
@@ -1537,8 +1572,14 @@ extern "C" int cdsgd_engine_step(cdsgd_engine* E, const float* g, void* stream) 
             }
             E->last_use[p] = t;
         } else {
-            rc = cdsgd_quantize(E->L, g, CDSGD_F32, E->d.residual[E->rcur], E->d.residual[E->rcur ^ 1], mine,
-                                E->d.alpha, E->d.err, tag, C);
+            if (E->d.residual_dtype == CDSGD_F32)
+                rc = cdsgd_quantize_f32r(E->L, g, static_cast<const float*>(E->d.residual[E->rcur]),
+                                         static_cast<float*>(E->d.residual[E->rcur ^ 1]), mine, E->d.alpha, E->d.err,
+                                         tag, C);
+            else
+                rc = cdsgd_quantize(E->L, g, CDSGD_F32, static_cast<const double*>(E->d.residual[E->rcur]),
+                                    static_cast<double*>(E->d.residual[E->rcur ^ 1]), mine, E->d.alpha, E->d.err, tag,
+                                    C);
         }
         prof_stop(E, pi, C);
         if (rc != CDSGD_OK) return rc;

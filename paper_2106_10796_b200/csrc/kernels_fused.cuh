@@ -23,8 +23,8 @@ enum { APPLY_Q = 0, APPLY_F = 1, APPLY_L = 2 };  // L: loc = W - eta_l*g only (W
 struct FusedArgs {
     // quantize(t)
     const float* g;
-    const double* r_in;
-    double* r_out;
+    const void* r_in;  // double* (exact) or float* (fp32-residual fast mode): the kernel's TR
+    void* r_out;
     uint32_t* words;   // local packed output when not exchanging
     double alpha;
     uint64_t tag;
@@ -62,16 +62,18 @@ struct FusedArgs {
 #ifndef CDSGD_FULL_SPEC
 #define CDSGD_FULL_SPEC 1
 #endif
-template <int NR, int APPLY, int CH, typename TW, bool FULL>
+template <int NR, int APPLY, int CH, typename TW, bool FULL, typename TR>
 __device__ __forceinline__ uint32_t fused_vec_task(const FusedArgs& a, const float* s_upd, const double* s_upd64,
                                                    int lane, int64_t e0, int64_t w0, int ne, int nw, int c0,
                                                    bool a_off, bool q_off, uint32_t ahi, uint32_t alo,
                                                    uint64_t& bad_idx, uint64_t& bad_sym, double& gsq, int& isq) {
     uint32_t myword = 0;
     TW* const W = static_cast<TW*>(a.W);
+    const TR* const r_in = static_cast<const TR*>(a.r_in);
+    TR* const r_out = static_cast<TR*>(a.r_out);
     float4 gv[CH], sv[CH];
     WV<TW> wv[CH];
-    d4 rv[CH];
+    WV<TR> rv[CH];
     uint32_t cw[APPLY == APPLY_Q ? NR : 1];
     if constexpr (APPLY == APPLY_Q) {
 #pragma unroll
@@ -83,7 +85,7 @@ __device__ __forceinline__ uint32_t fused_vec_task(const FusedArgs& a, const flo
         const int64_t e = e0 + 128 * (c0 + c) + 4 * lane;
         const int nv = FULL ? 4 : nvalid4(ne, 128 * (c0 + c) + 4 * lane);
         gv[c] = ld_stream_m(a.g + e, nv);
-        rv[c] = ld_stream_m(a.r_in + e, nv);
+        ldw4(r_in + e, nv, rv[c]);
         ldw4(W + e, nv, wv[c]);
         if constexpr (APPLY == APPLY_F) sv[c] = ld_stream_m(a.gsum + e, nv);
     }
@@ -95,7 +97,7 @@ __device__ __forceinline__ uint32_t fused_vec_task(const FusedArgs& a, const flo
         const int nv = FULL ? 4 : nvalid4(ne, 128 * (c0 + c) + 4 * lane);
         float g4[4] = {gv[c].x, gv[c].y, gv[c].z, gv[c].w};
         WV<TW>& w4 = wv[c];
-        double r4[4] = {rv[c].x, rv[c].y, rv[c].z, rv[c].w};
+        const TR(&r4)[4] = rv[c].v;
         if (!a_off) {
             float l4[4];
             if constexpr (APPLY == APPLY_Q) {
@@ -135,11 +137,11 @@ __device__ __forceinline__ uint32_t fused_vec_task(const FusedArgs& a, const flo
             st_stream_m(a.loc + e, l4[0], l4[1], l4[2], l4[3], nv);
         }
         if (!q_off) {
-            double o[4];
+            TR o[4];
             uint32_t code = 0;
 #pragma unroll
             for (int q = 0; q < 4; ++q) code |= quant1_lean(r4[q], g4[q], a.alpha, ahi, alo, o[q], bad) << (2 * q);
-            st_stream_m(a.r_out + e, o[0], o[1], o[2], o[3], nv);
+            st_stream_m(r_out + e, o[0], o[1], o[2], o[3], nv);
             v[c] = code << (8 * (lane & 3));
         } else {
             v[c] = 0;
@@ -149,10 +151,10 @@ __device__ __forceinline__ uint32_t fused_vec_task(const FusedArgs& a, const flo
 #pragma unroll
         for (int c = 0; c < CH; ++c) {
             const float g4[4] = {gv[c].x, gv[c].y, gv[c].z, gv[c].w};
-            const double r4[4] = {rv[c].x, rv[c].y, rv[c].z, rv[c].w};
+            const TR(&r4)[4] = rv[c].v;
 #pragma unroll
             for (int q = 0; q < 4; ++q)
-                if (nonfinite(__dadd_rn(r4[q], static_cast<double>(g4[q])))) {
+                if (nonfinite(r4[q] + static_cast<TR>(g4[q]))) {
                     const uint64_t idx =
                         a.tag | static_cast<uint64_t>(e0 + 128 * (c0 + c) + 4 * lane + q);
                     bad_idx = idx < bad_idx ? idx : bad_idx;
@@ -183,7 +185,7 @@ __device__ __forceinline__ uint32_t fused_vec_task(const FusedArgs& a, const flo
 #ifndef CDSGD_F64_CH
 #define CDSGD_F64_CH 4
 #endif
-template <int NR, int APPLY, int CH = CHUNKS, typename TW = float>
+template <int NR, int APPLY, int CH = CHUNKS, typename TW = float, typename TR = double>
 __global__ void __launch_bounds__(256, sizeof(TW) == 8 ? CDSGD_F64_MINB : 2) k_fused_ldg(FusedArgs a, KeyTab kt, DecodeTab tab) {
     constexpr int SPL = CHUNKS / CH;  // tasks per tile
     __shared__ float s_upd[2 * MAX_RANKS + 1];
@@ -257,17 +259,17 @@ __global__ void __launch_bounds__(256, sizeof(TW) == 8 ? CDSGD_F64_MINB : 2) k_f
             const int ne = ne64 < TILE_ELEMS ? static_cast<int>(ne64) : TILE_ELEMS;
             const int64_t nw64 = cc.w1 - w0;
             const int nw = nw64 < TILE_WORDS ? static_cast<int>(nw64) : TILE_WORDS;
-            const bool fast = aligned_to(a.g + e0, 16) && aligned_to(a.r_in + e0, 32) &&
-                              aligned_to(a.r_out + e0, 32) && aligned_to(W + e0, 4 * sizeof(TW)) && aligned_to(a.loc + e0, 16) &&
+            const bool fast = aligned_to(a.g + e0, 16) && aligned_to(static_cast<const TR*>(a.r_in) + e0, 4 * sizeof(TR)) &&
+                              aligned_to(static_cast<TR*>(a.r_out) + e0, 4 * sizeof(TR)) && aligned_to(W + e0, 4 * sizeof(TW)) && aligned_to(a.loc + e0, 16) &&
                               (APPLY != APPLY_F || aligned_to(a.gsum + e0, 16)) && (APPLY != APPLY_Q || a.exact);
             if (!fast && c0 != 0) continue;  // misaligned tiles: one task does the whole tile
             uint32_t myword = 0;
             if (fast) {
                 if (CDSGD_FULL_SPEC && ne == TILE_ELEMS)
-                    myword = fused_vec_task<NR, APPLY, CH, TW, true>(a, s_upd, s_upd64, lane, e0, w0, ne, nw, c0, a_off,
+                    myword = fused_vec_task<NR, APPLY, CH, TW, true, TR>(a, s_upd, s_upd64, lane, e0, w0, ne, nw, c0, a_off,
                                                                      q_off, ahi, alo, bad_idx, bad_sym, gsq, isq);
                 else
-                    myword = fused_vec_task<NR, APPLY, CH, TW, false>(a, s_upd, s_upd64, lane, e0, w0, ne, nw, c0, a_off,
+                    myword = fused_vec_task<NR, APPLY, CH, TW, false, TR>(a, s_upd, s_upd64, lane, e0, w0, ne, nw, c0, a_off,
                                                                       q_off, ahi, alo, bad_idx, bad_sym, gsq, isq);
             } else {
                 uint32_t cw[APPLY == APPLY_Q ? NR : 1];
@@ -318,10 +320,10 @@ __global__ void __launch_bounds__(256, sizeof(TW) == 8 ? CDSGD_F64_MINB : 2) k_f
                             a.loc[e] = loc_of(wn, gval, a.eta_l, a.eta_l_d);
                         }
                         if (!q_off) {
-                            double o;
+                            TR o;
                             bool b;
-                            const uint32_t code = quant1(a.r_in[e], gval, a.alpha, o, b);
-                            a.r_out[e] = o;
+                            const uint32_t code = quant1(static_cast<const TR*>(a.r_in)[e], gval, a.alpha, o, b);
+                            static_cast<TR*>(a.r_out)[e] = o;
                             p = code == 1u;
                             m = code == 2u;
                             if (b) {

@@ -77,13 +77,13 @@ __device__ __forceinline__ void lds4(const double* chunk, int lane, double (&v)[
 // CTA = WARPS warps, one CTA per SM (the smem ring, not occupancy, hides latency).
 
 // ================================================================ K1 (TMA)
-template <typename G>
-__device__ __noinline__ uint64_t rescan_nonfinite(const G* sg, const double* sr, int lane, int64_t e0, uint64_t tag,
+template <typename G, typename TR>
+__device__ __noinline__ uint64_t rescan_nonfinite(const G* sg, const TR* sr, int lane, int64_t e0, uint64_t tag,
                                                   uint64_t bad_idx) {
     for (int c = 0; c < CHUNKS; ++c)
         for (int q = 0; q < 4; ++q) {
             const int el = 128 * c + 4 * lane + q;
-            if (nonfinite(__dadd_rn(sr[el], static_cast<double>(sg[el])))) {
+            if (nonfinite(sr[el] + static_cast<TR>(sg[el]))) {
                 const uint64_t idx = tag | static_cast<uint64_t>(e0 + el);
                 bad_idx = idx < bad_idx ? idx : bad_idx;
             }
@@ -91,20 +91,20 @@ __device__ __noinline__ uint64_t rescan_nonfinite(const G* sg, const double* sr,
     return bad_idx;
 }
 
-template <typename G, int WARPS, int S>
+template <typename G, int WARPS, int S, typename TR = double>
 struct QuantSmem {
     static constexpr int GB = TILE_ELEMS * sizeof(G);
-    static constexpr int RB = TILE_ELEMS * 8;
+    static constexpr int RB = TILE_ELEMS * sizeof(TR);
     static constexpr int SLOT = GB + RB;
     static constexpr int WARP = S * SLOT;
     static constexpr int BYTES = WARPS * WARP + WARPS * S * 8;
 };
 
-template <typename G, int WARPS, int S>
+template <typename G, int WARPS, int S, typename TR = double>
 __global__ void __launch_bounds__(WARPS * 32, 1)
-    k_quantize_tma(const G* __restrict__ g, const double* r_in, double* r_out, uint32_t* __restrict__ words,
+    k_quantize_tma(const G* __restrict__ g, const TR* r_in, TR* r_out, uint32_t* __restrict__ words,
                    KeyTab kt, double alpha, uint64_t* err, uint64_t tag, P2PArgs x) {
-    using SM = QuantSmem<G, WARPS, S>;
+    using SM = QuantSmem<G, WARPS, S, TR>;
     extern __shared__ __align__(128) unsigned char smem[];
     pdl_enter(nullptr, nullptr);
     const bool peer_failed = p2p_wait(x);  // fused exchange: peers have released the slot we are about to fill
@@ -133,7 +133,8 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
         pc.advance_to(kt, ti);
         const int64_t e0 = pc.e0 + (ti - pc.t0) * TILE_ELEMS;
         const bool full = pc.e1 - e0 >= TILE_ELEMS;
-        const bool ok = full && aligned_to(g + e0, 16) && aligned_to(r_in + e0, 16) && aligned_to(r_out + e0, 32);
+        const bool ok = full && aligned_to(g + e0, 16) && aligned_to(r_in + e0, 16) &&
+                        aligned_to(r_out + e0, 4 * sizeof(TR));
         if (ok) {
             if (lane == 0) {
                 unsigned char* sl = ring + slot * SM::SLOT;
@@ -166,10 +167,10 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
             tma::wait(&bars[slot], (phase >> slot) & 1u);
             phase ^= 1u << slot;
             const G* sg = reinterpret_cast<const G*>(ring + slot * SM::SLOT);
-            const double* sr = reinterpret_cast<const double*>(ring + slot * SM::SLOT + SM::GB);
+            const TR* sr = reinterpret_cast<const TR*>(ring + slot * SM::SLOT + SM::GB);
             // phase A: every smem read of the tile first (one dependency level)
             G gv[CHUNKS][4];
-            double rv[CHUNKS][4];
+            TR rv[CHUNKS][4];
 #pragma unroll
             for (int c = 0; c < CHUNKS; ++c) {
                 tma::lds4(sg + 128 * c, lane, gv[c]);
@@ -182,7 +183,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
             const uint32_t alo = static_cast<uint32_t>(__double2loint(alpha));
 #pragma unroll
             for (int c = 0; c < CHUNKS; ++c) {
-                double o[4];
+                TR o[4];
                 uint32_t code = 0;
 #pragma unroll
                 for (int q = 0; q < 4; ++q) code |= quant1_lean(rv[c][q], gv[c][q], alpha, ahi, alo, o[q], bad) << (2 * q);
@@ -207,7 +208,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
                 const int el = 32 * s + lane;
                 bool p = false, m = false;
                 if (el < ne) {
-                    double o;
+                    TR o;
                     bool b;
                     const uint32_t code = quant1(r_in[e0 + el], g[e0 + el], alpha, o, b);
                     r_out[e0 + el] = o;

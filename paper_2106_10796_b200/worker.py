@@ -62,6 +62,7 @@ class CDSGDWorker:
         exchange: str = "p2p",
         group=None,
         weights: str = "f64",
+        residual: str = "f64",
     ):
         if not torch.cuda.is_available():
             raise _lib.LibraryError("CDSGDWorker needs a CUDA device (no CPU fallback)")
@@ -85,11 +86,15 @@ class CDSGDWorker:
         if weights not in _lib.WEIGHTS:
             raise ConfigError(f"weights must be 'f64' (exact) or 'f32' (fast), got {weights!r}")
         self.weights_dtype = weights
+        if residual not in _lib.RESIDUAL or (residual == "f32" and weights != "f32"):
+            raise ConfigError("residual must be 'f64' (exact) or 'f32' (fast mode, with weights='f32')")
+        self.residual_dtype = residual
+        rt = torch.float64 if residual == "f64" else torch.float32
         wt = torch.float64 if weights == "f64" else torch.float32
         with torch.cuda.device(dev):
             self.W = w0.reshape(-1).to(device=dev, dtype=wt).clone()
             self.loc = w0.reshape(-1).to(device=dev, dtype=torch.float32).clone()
-            self.residuals = [torch.zeros(n, dtype=torch.float64, device=dev), torch.empty(n, dtype=torch.float64, device=dev)]
+            self.residuals = [torch.zeros(n, dtype=rt, device=dev), torch.empty(n, dtype=rt, device=dev)]
             self.gathered = [torch.zeros(self.world * nw, dtype=torch.int32, device=dev).view(torch.uint32) for _ in range(2)]
             self.gsum = [torch.empty(n, dtype=torch.float32, device=dev) for _ in range(2)] if self.world > 1 else [None, None]
             self.err = torch.full((2,), -1, dtype=torch.int64, device=dev)
@@ -105,6 +110,7 @@ class CDSGDWorker:
             d.bypass_local = int(bypass_local)
             d.gnorm_ring = self.gnorm_ring
             d.weights_dtype = _lib.WEIGHTS[weights]
+            d.residual_dtype = _lib.RESIDUAL[residual]
             d.alpha = float(hp.alpha)
             d.eta_global = float(hp.eta_global)
             d.eta_local = float(hp.local_lr)
@@ -180,7 +186,7 @@ class CDSGDWorker:
 
     @property
     def residual(self) -> torch.Tensor:
-        """The live fp64 residual (concatenated over keys)."""
+        """The live residual (concatenated over keys): fp64, or fp32 in the fast mode."""
         return self.residuals[self.state().residual_index]
 
     @property

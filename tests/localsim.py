@@ -98,7 +98,7 @@ class LocalSim:
         r = self.res[w]
         c = self.rcur[w]
         _lib.check(self.lib.cdsgd_fused_round(
-            self.lay, g.data_ptr(), r[c].data_ptr(), r[c ^ 1].data_ptr(), slot.data_ptr() + 4 * w * self.nw,
+            self.lay, g.data_ptr(), r[c].data_ptr(), r[c ^ 1].data_ptr(), _lib.F64, slot.data_ptr() + 4 * w * self.nw,
             self.alpha, self.err[w].data_ptr(), 0, self.W[w].data_ptr(), self.wdt, self.loc[w].data_ptr(),
             gathered.data_ptr() if gathered is not None else None, self.N, self.nw, self.eta_g, self.eta_l, 0,
             gnorm.data_ptr() if gnorm is not None else None, self._st()), "fused_round")
