@@ -612,7 +612,8 @@ def run_ours(args):
     waits = {k: {"launches": prof[k]["n"], "avg_us": 1e3 * prof[k]["ms"] / prof[k]["n"]}
              for k in ("wait",) if prof[k]["n"]}
     roof = {"bound": "hbm", "kernel": dom, "achieved": kernels[dom]["achieved_gbs"], "peak": peak, "unit": "GB/s",
-            "frac": kernels[dom]["achieved_gbs"] / peak, "traffic": ncu_traffic(args.workload, dom),
+            "frac": kernels[dom]["achieved_gbs"] / peak,
+            "traffic": ncu_traffic(args.workload + ("" if args.weights == "f64" else "_f32w"), dom),
             "algorithmic_bytes_per_launch": alg[dom], "peak_source": peak_src}
     exch = None
     if world > 1:

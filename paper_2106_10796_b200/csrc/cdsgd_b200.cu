@@ -586,13 +586,21 @@ int launch_apply_full(void* W, int wdt, const float* gsum, int nr, int64_t n, do
     return CDSGD_OK;
 }
 // Fused apply(t-1) + quantize(t), register-staged (measured faster than a TMA-ring variant).
+// Chunk-sized tasks (CH=1) below this many whole tiles per resident warp (CDSGD_CH1_TPW; 0 = never)
+int ch1_tiles_per_warp() {
+    static const int v = [] {
+        const char* e = getenv("CDSGD_CH1_TPW");
+        return e != nullptr ? atoi(e) : 2;
+    }();
+    return v;
+}
 template <int NR, int AP, typename TW, typename TR>
 int launch_fused_cfg(const FusedArgs& a, const KeyTab& kt, const DecodeTab& tab, cudaStream_t st) {
     constexpr int CHL = sizeof(TW) == 8 ? CDSGD_F64_CH : CHUNKS;  // chunks per task on large layouts
     // fewer than 2 whole-tile tasks per resident warp: split tiles into chunk tasks
     const int64_t warps =
         static_cast<int64_t>(resident_blocks(k_fused_ldg<NR, AP, CHL, TW, TR>, THREADS)) * WARPS_PER_BLOCK;
-    if (kt.ntiles < 2 * warps)
+    if (kt.ntiles < ch1_tiles_per_warp() * warps)
         launch_pdl(k_fused_ldg<NR, AP, 1, TW, TR>, tile_grid(k_fused_ldg<NR, AP, 1, TW, TR>, kt.ntiles * CHUNKS), THREADS,
                    0, st, a, kt, tab);
     else

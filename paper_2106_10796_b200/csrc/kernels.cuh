@@ -670,9 +670,6 @@ __device__ __forceinline__ void apply_vec_tile(const ApplyQArgs& a, const float*
 #endif
 template <int NR, int WIDE = 0, typename TW = float>
 __global__ void __launch_bounds__(WIDE ? 512 : 256, WIDE ? 1 : CDSGD_K2_MINB) k_apply_quant(ApplyQArgs a, KeyTab kt, DecodeTab tab) {
-    pdl_enter(a.gclear[0], a.gclear[1]);
-    const bool peer_failed = p2p_wait2(a.x, a.xs);
-    const bool skip = peer_failed || (a.err != nullptr && *reinterpret_cast<volatile uint64_t*>(a.err) < a.skip_below);
     __shared__ double s_mean[2 * MAX_RANKS + 1];
     __shared__ double s_upd64[2 * MAX_RANKS + 1];
     __shared__ float s_upd[2 * MAX_RANKS + 1];
@@ -683,7 +680,6 @@ __global__ void __launch_bounds__(WIDE ? 512 : 256, WIDE ? 1 : CDSGD_K2_MINB) k_
         s_upd[threadIdx.x] = tab.upd[threadIdx.x];
         s_upd64[threadIdx.x] = tab.upd64[threadIdx.x];
     }
-    __syncthreads();
     int64_t tb, te;
     warp_range(kt.ntiles, tb, te);
     const int lane = threadIdx.x & 31;
@@ -705,9 +701,14 @@ __global__ void __launch_bounds__(WIDE ? 512 : 256, WIDE ? 1 : CDSGD_K2_MINB) k_
         cend = tb + (int64_t)CLAIM < kt.ntiles ? tb + (int64_t)CLAIM : kt.ntiles;
         te = tb < kt.ntiles ? kt.ntiles : tb;
     }
+    // constant inputs (tables, schedule, key seek) before griddepcontrol.wait (see k_fused_ldg)
+    TileCursor kc;
+    if (tb < te) kc.seek_warp(kt, tb, lane);
+    pdl_enter(a.gclear[0], a.gclear[1]);
+    const bool peer_failed = p2p_wait2(a.x, a.xs);
+    const bool skip = peer_failed || (a.err != nullptr && *reinterpret_cast<volatile uint64_t*>(a.err) < a.skip_below);
+    __syncthreads();
     if (tb < te && !skip) {
-        TileCursor kc;
-        kc.seek_warp(kt, tb, lane);
         for (int64_t ti = tb; ti < te; ++ti) {
             if (dyn && ti >= cend) {
                 const unsigned cl = ti < tail_from ? CLAIM : 1u;

@@ -191,19 +191,9 @@ __global__ void __launch_bounds__(256, sizeof(TW) == 8 ? CDSGD_F64_MINB : 2) k_f
     __shared__ float s_upd[2 * MAX_RANKS + 1];
     __shared__ double s_upd64[2 * MAX_RANKS + 1];
     TW* const W = static_cast<TW*>(a.W);
-    pdl_enter(a.gclear[0], a.gclear[1]);
-    const bool peer_failed = p2p_wait2(a.xq, a.xa);
-    const uint64_t e0v = a.err != nullptr ? *reinterpret_cast<volatile uint64_t*>(a.err) : ~0ull;
-    // sticky abort: only an error of an EARLIER round (smaller tag) stops the quantize, so a
-    // non-finite value found by one CTA never suppresses the scan of the others in this launch
-    // (the reported index stays the first non-finite element, codec.py:182-185)
-    const bool q_off = e0v < a.tag || peer_failed;
-    const bool a_off = e0v < a.skip_below || peer_failed;
-    if (APPLY == APPLY_Q && threadIdx.x < 2 * NR + 1) {
-        s_upd[threadIdx.x] = tab.upd[threadIdx.x];
-        s_upd64[threadIdx.x] = tab.upd64[threadIdx.x];
-    }
-    __syncthreads();
+    // Everything that reads only constant inputs (decode table, key table, schedule) runs
+    // BEFORE griddepcontrol.wait, overlapping the previous kernel's tail: on launch-bound
+    // layouts the key seek (two dependent key-table loads) was part of every round's latency.
     const int lane = threadIdx.x & 31;
     const uint32_t ahi = static_cast<uint32_t>(__double2hiint(a.alpha));
     const uint32_t alo = static_cast<uint32_t>(__double2loint(a.alpha));
@@ -233,9 +223,22 @@ __global__ void __launch_bounds__(256, sizeof(TW) == 8 ? CDSGD_F64_MINB : 2) k_f
         tb = cbase;
         te = cbase < ntasks ? ntasks : cbase;  // loop bound; real bound checked per claim
     }
+    if (APPLY == APPLY_Q && threadIdx.x < 2 * NR + 1) {
+        s_upd[threadIdx.x] = tab.upd[threadIdx.x];
+        s_upd64[threadIdx.x] = tab.upd64[threadIdx.x];
+    }
+    TileCursor cc;
+    if (tb < te) cc.seek_warp(kt, tb / SPL, lane);
+    pdl_enter(a.gclear[0], a.gclear[1]);  // from here on: memory the preceding kernels write
+    const bool peer_failed = p2p_wait2(a.xq, a.xa);
+    const uint64_t e0v = a.err != nullptr ? *reinterpret_cast<volatile uint64_t*>(a.err) : ~0ull;
+    // sticky abort: only an error of an EARLIER round (smaller tag) stops the quantize, so a
+    // non-finite value found by one CTA never suppresses the scan of the others in this launch
+    // (the reported index stays the first non-finite element, codec.py:182-185)
+    const bool q_off = e0v < a.tag || peer_failed;
+    const bool a_off = e0v < a.skip_below || peer_failed;
+    __syncthreads();
     if (tb < te) {
-        TileCursor cc;
-        cc.seek_warp(kt, tb / SPL, lane);
         for (int64_t task = tb; task < te; ++task) {
             if (dyn) {
                 if (task >= cend) {  // claim the next batch (single tasks in the last ~one per warp)

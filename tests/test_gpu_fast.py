@@ -104,4 +104,5 @@ def test_fast_mode_needs_fp32_weights(lib):
     from paper_2106_10796_b200.worker import CDSGDWorker
 
     with pytest.raises(ConfigError):
-        CDSGDWorker(Layout.from_lengths([64]), HyperParams(workers=1), np.zeros(64, np.float32), residual="f32")
+        CDSGDWorker(Layout.from_lengths([64]), HyperParams(algo="cdsgd", workers=1), np.zeros(64, np.float32),
+                    residual="f32")
