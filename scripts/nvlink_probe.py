@@ -22,6 +22,21 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 
+def smi_nvlink(idx):
+    """Fallback: `nvidia-smi nvlink -gt d` (data throughput counters, KiB per link)."""
+    import re
+    import subprocess
+
+    try:
+        out = subprocess.run(["nvidia-smi", "nvlink", "-gt", "d", "-i", str(idx)], capture_output=True, text=True,
+                             timeout=30).stdout
+    except (OSError, subprocess.TimeoutExpired):
+        return None, ""
+    tx = sum(int(x) for x in re.findall(r"Tx\w*:\s*(\d+)\s*KiB", out))
+    rx = sum(int(x) for x in re.findall(r"Rx\w*:\s*(\d+)\s*KiB", out))
+    return ([tx, rx] if (tx or rx) else None), out
+
+
 def nvlink_kib(handle):
     import pynvml as N
 
@@ -90,6 +105,9 @@ def main():
     dist.barrier(device_ids=[local])
     torch.cuda.synchronize(dev)
     c0 = nvlink_kib(handle)
+    s0, raw0 = (None, "")
+    if c0 is None:
+        s0, raw0 = smi_nvlink(local)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for i in range(args.rounds):
@@ -98,6 +116,9 @@ def main():
     e1.record()
     e1.synchronize()
     c1 = nvlink_kib(handle)
+    if c0 is None:
+        s1, raw1 = smi_nvlink(local)
+        c0, c1 = s0, s1
     ms = e0.elapsed_time(e1)
     wk.check()
     P = 4 * nw
@@ -113,7 +134,8 @@ def main():
                     "note": "NVML data counters include protocol overhead (flits/headers) and the flag "
                             "traffic; they count every NVLink transfer of the process in the window"})
     else:
-        res["nvlink_counters"] = "NVML NVLink throughput fields unavailable"
+        res["nvlink_counters"] = "unavailable (NVML throughput fields and nvidia-smi nvlink -gt d)"
+        res["nvidia_smi_nvlink_raw"] = raw0[:600]
     allres = [None] * world
     dist.all_gather_object(allres, res)
     if rank == 0:
