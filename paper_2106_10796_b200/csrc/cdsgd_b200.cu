@@ -809,6 +809,14 @@ struct cdsgd_engine {
     bool pcorr = false;                // P2P mode: correction rounds by the exact sharded NVLink reduce
     bool plain_after_ar = false;       // plain (non-PDL) launch of the apply beside a correction all-reduce
     int reserve_sms = 0;               // SMs left free for the all-reduce's CTAs (CDSGD_RESERVE_SMS)
+    // NCCL symmetric-window correction all-reduce (CDSGD_NCCL_SYM=1, p2p mode): g_t staged into an
+    // ncclMemAlloc'ed, window-registered buffer (by K2, which streams g_t anyway), all-reduced into a
+    // registered gsum buffer with NCCL's symmetric-memory kernels. Parity-green but measured slower
+    // at N=2 (200 Gelem/s, 232 with NCCL_NVLS_ENABLE=0, vs 252 for the default split): an option.
+    bool nccl_sym = false;
+    void* sym_stage[2] = {nullptr, nullptr};
+    void* sym_gsum[2] = {nullptr, nullptr};
+    ncclWindow_t win[4] = {nullptr, nullptr, nullptr, nullptr};
     int64_t ar_round = -1;             // correction round whose all-reduce is in flight on the exchange streams
     bool diag_local_codes = false;     // timing diagnostic: store codes only locally
     bool diag_no_wait = false;         // timing diagnostic: skip the code-exchange flag waits
@@ -1102,6 +1110,29 @@ int p2p_reduce_async(cdsgd_engine* E, int64_t t, cudaStream_t C) {
     return CDSGD_OK;
 }
 
+// NCCL symmetric-window correction all-reduce of round t (CDSGD_NCCL_SYM): stage g_t into the
+// registered buffer unless K2 already did, then all-reduce it on the exchange stream after
+// everything on C (the staging) — evX[t] marks completion for K3(t).
+int sym_allreduce(cdsgd_engine* E, int64_t t, const float* g, bool staged, cudaStream_t C) {
+    const int s = static_cast<int>(t & 1);
+    const size_t bytes = 4 * static_cast<size_t>(E->L->n);
+    if (!staged) CUDA_TRY(cudaMemcpyAsync(E->sym_stage[s], g, bytes, cudaMemcpyDeviceToDevice, C));
+    CUDA_TRY(cudaEventRecord(E->evQ[s], C));
+    CUDA_TRY(cudaStreamWaitEvent(E->xs, E->evQ[s], 0));
+    const long pi = prof_start(E, 4, E->xs);
+    NCCL_TRY(ncclAllReduce(E->sym_stage[s], E->d.gsum[s], static_cast<size_t>(E->L->n), ncclFloat, ncclSum,
+                           E->comm->nccl, E->xs));
+    prof_stop(E, pi, E->xs);
+    CUDA_TRY(cudaEventRecord(E->evX[s], E->xs));
+    return CDSGD_OK;
+}
+StageDst sym_stage_dst(const cdsgd_engine* E, int64_t t) {
+    StageDst d{};
+    d.chunk = std::max<int64_t>(E->L->n, TILE_ELEMS) + 4;  // one "owner": element e lands at base[0] + e
+    d.base[0] = static_cast<float*>(E->sym_stage[t & 1]);
+    return d;
+}
+
 // Finish round p: wait for its exchange, then K2 (codes) or K3 (full) fused with
 // the local update from g_next (nullable).
 int engine_apply(cdsgd_engine* E, int64_t p, bool comp, const float* gp, const float* gnext, cudaStream_t C,
@@ -1341,6 +1372,23 @@ extern "C" int cdsgd_engine_attach_p2p(cdsgd_engine* E, void* const* peer_bases,
         const char* nf = getenv("CDSGD_NO_FUSE");
         E->fuse = !(nf != nullptr && nf[0] == '1');
     }
+    {
+        const char* ns = getenv("CDSGD_NCCL_SYM");
+        if (ns != nullptr && ns[0] == '1' && !exact_correction && E->comm != nullptr) {
+            const size_t bytes = 4 * static_cast<size_t>(E->L->n);
+            for (int i = 0; i < 2; ++i) {
+                NCCL_TRY(ncclMemAlloc(&E->sym_stage[i], bytes));
+                NCCL_TRY(ncclMemAlloc(&E->sym_gsum[i], bytes));
+                NCCL_TRY(ncclCommWindowRegister(E->comm->nccl, E->sym_stage[i], bytes, &E->win[2 * i],
+                                                NCCL_WIN_COLL_SYMMETRIC));
+                NCCL_TRY(ncclCommWindowRegister(E->comm->nccl, E->sym_gsum[i], bytes, &E->win[2 * i + 1],
+                                                NCCL_WIN_COLL_SYMMETRIC));
+                E->d.gsum[i] = static_cast<float*>(E->sym_gsum[i]);
+            }
+            E->nccl_sym = true;
+            E->ce_frac = 0.0;
+        }
+    }
     return CDSGD_OK;
 }
 
@@ -1388,6 +1436,12 @@ extern "C" int cdsgd_engine_destroy(cdsgd_engine* E) {
     }
     if (E->xs) cudaStreamDestroy(E->xs);
     if (E->xs2) cudaStreamDestroy(E->xs2);
+    for (int i = 0; i < 4; ++i)
+        if (E->win[i] != nullptr && E->comm != nullptr) ncclCommWindowDeregister(E->comm->nccl, E->win[i]);
+    for (int i = 0; i < 2; ++i) {
+        if (E->sym_stage[i]) ncclMemFree(E->sym_stage[i]);
+        if (E->sym_gsum[i]) ncclMemFree(E->sym_gsum[i]);
+    }
     if (E->counters) cudaFree(E->counters);
     if (E->gacc) cudaFree(E->gacc);
     if (E->sched) cudaFree(E->sched);
@@ -1618,6 +1672,8 @@ extern "C" int cdsgd_engine_step(cdsgd_engine* E, const float* g, void* stream) 
         CUDA_TRY(cudaEventRecord(E->evC, E->xs2));
         CUDA_TRY(cudaStreamWaitEvent(E->xs, E->evC, 0));
         CUDA_TRY(cudaEventRecord(E->evX[t & 1], E->xs));
+    } else if (E->xused[t & 1] && !comp && E->nccl_sym) {
+        // deferred until after the apply below, which stages g_t into the registered buffer
     } else if (E->xused[t & 1]) {
         CUDA_TRY(cudaEventRecord(E->evQ[t & 1], C));
         CUDA_TRY(cudaStreamWaitEvent(E->xs, E->evQ[t & 1], 0));
@@ -1638,8 +1694,13 @@ extern "C" int cdsgd_engine_step(cdsgd_engine* E, const float* g, void* stream) 
     if (E->xused[t & 1] && !comp) E->ar_round = t;
     const ReserveScope reserve3(E->xused[t & 1] && !comp ? E->reserve_sms : 0);
     const bool sync_path = !E->uses_local || t < E->n_warmup - 1;
+    const bool sym_ar = E->xused[t & 1] && !comp && E->nccl_sym;
     if (sync_path) {
         if (E->pending) return fail(CDSGD_ERR_STATE, "internal: pending round on the synchronous path");
+        if (sym_ar) {
+            rc = sym_allreduce(E, t, g, false, C);
+            if (rc != CDSGD_OK) return rc;
+        }
         if (!comp && E->p2p && E->pcorr) {
             rc = p2p_stage(E, t, g, C);
             if (rc != CDSGD_OK) return rc;
@@ -1664,6 +1725,12 @@ extern "C" int cdsgd_engine_step(cdsgd_engine* E, const float* g, void* stream) 
             E->compute_is_loc = true;
             E->t = t + 1;
             return CDSGD_OK;
+        } else if (E->pending && sym_ar && E->pend_comp) {
+            // K2(t-1) streams g_t for the local update anyway: it also stages it for the all-reduce
+            const StageDst dst = sym_stage_dst(E, t);
+            rc = engine_apply(E, E->pend_t, E->pend_comp, E->pend_grad, g, C, &dst, nullptr);
+            if (rc == CDSGD_OK) rc = sym_allreduce(E, t, g, true, C);
+            staged = true;
         } else if (E->pending) {
             rc = engine_apply(E, E->pend_t, E->pend_comp, E->pend_grad, g, C);
         } else {
@@ -1674,6 +1741,10 @@ extern "C" int cdsgd_engine_step(cdsgd_engine* E, const float* g, void* stream) 
             prof_stop(E, pi, C);
         }
         if (rc != CDSGD_OK) return rc;
+        if (sym_ar && !staged) {
+            rc = sym_allreduce(E, t, g, false, C);
+            if (rc != CDSGD_OK) return rc;
+        }
         if (!comp && E->p2p && E->pcorr && !staged) {  // after apply(t-1) finished writing W: peers may target it
             rc = p2p_stage(E, t, g, C);
             if (rc != CDSGD_OK) return rc;

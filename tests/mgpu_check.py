@@ -77,6 +77,45 @@ def run_case(case, exchange, comm, rank, world, dev):
     wk.close()
 
 
+def run_pipelined_case(exchange, comm, rank, world, dev):
+    """the overlapped paths under real concurrency with caller kernels. An 8.4M-
+    element layout (so the default copy-engine share of the correction all-reduce is on),
+    k=4, 12 rounds issued back to back with NO host sync between them and a caller compute
+    kernel (a matmul) on the same stream between steps — then flush and compare: residual
+    bitwise and W within tolerance against the C restatement over EVERY element, W
+    replicas bitwise across ranks."""
+    from oracle import cpu_port
+
+    sizes = [8_388_608, 4099, 33]
+    layout = Layout.from_lengths(sizes)
+    n, T = layout.total, 12
+    hp = HyperParams(algo="cdsgd", workers=world, eta_global=0.1, eta_local=0.4, k=4, alpha=0.5, warmup_n=0)
+    w0 = O.synthetic_weights(8, n)
+    grads = [torch.from_numpy(O.synthetic_grad(8, t, rank, n)).to(dev) for t in range(T)]
+    a = torch.randn(2048, 2048, device=dev)
+    wk = CDSGDWorker(layout, hp, w0, rank=rank, comm=comm, exchange=exchange)
+    torch.cuda.synchronize(dev)
+    for t in range(T):
+        for _ in range(4):
+            a = torch.tanh(a @ a * 1e-3)  # caller compute on the same stream, between rounds
+        wk.step(grads[t])
+    wk.flush()
+    W = wk.weights.clone()
+    allW = [torch.empty_like(W) for _ in range(world)]
+    dist.all_gather(allW, W)
+    for w in range(world):
+        assert torch.equal(allW[w], W), f"{exchange}: W replica of rank {w} differs (pipelined)"
+    if cpu_port.load() is None:
+        return
+    port = cpu_port.CPortEngine(w0.astype(np.float64), sizes, world, k=4, alpha=0.5)
+    for t in range(T):
+        port.step(np.stack([O.synthetic_grad(8, t, w, n) for w in range(world)]))
+    assert np.array_equal(wk.residual.cpu().numpy().view(np.uint64), port.res[rank].view(np.uint64)), \
+        f"{exchange} rank {rank}: residual (pipelined)"
+    np.testing.assert_allclose(W.cpu().numpy(), port.W, rtol=RTOL, atol=ATOL, err_msg=f"{exchange} W (pipelined)")
+    wk.close()
+
+
 def run_records_case(exchange, comm, rank, world, dev):
     """World 2: per-round records (records.Recorder) vs the reference's own metrics.csv
     (tests/golden/metrics_n2.csv, unmodified reference: make_metrics_golden.py)."""
@@ -143,6 +182,7 @@ def main():
             run_case(case, exchange, comm, rank, world, dev)
         if world == 2:
             run_records_case(exchange, comm, rank, world, dev)
+        run_pipelined_case(exchange, comm, rank, world, dev)
         if exchange in ("p2p", "p2p-exact"):
             run_failure_case(exchange, comm, rank, world, dev)
     comm.close()
