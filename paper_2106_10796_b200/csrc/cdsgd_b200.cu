@@ -13,6 +13,8 @@
 #include <cstring>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: a no-op unless a profiler is attached
+
 #include "cdsgd_b200.h"
 #include "kernels.cuh"
 #include "kernels_tma.cuh"
@@ -1457,8 +1459,18 @@ extern "C" int cdsgd_engine_round_compressed(const cdsgd_engine* E, int64_t t) {
     return c ? 1 : 0;
 }
 
+// NVTX range per engine step, named by the round's kind (host-side phase markers for nsys-style
+// timelines: "cdsgd round (compressed)" / "(correction)")
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
+
 extern "C" int cdsgd_engine_step(cdsgd_engine* E, const float* g, void* stream) {
     if (E == nullptr || g == nullptr) return fail(CDSGD_ERR_ARG, "NULL argument");
+    bool comp_ = false;
+    round_compressed(E, E->t, &comp_);
+    const NvtxRange nvtx_(comp_ ? "cdsgd round (compressed)" : "cdsgd round (correction / full)");
     if (E->failed) return fail(CDSGD_ERR_STATE, "engine failed at an earlier round; see cdsgd_engine_check");
     if (E->t - E->err_base >= (int64_t(1) << 23))
         return fail(CDSGD_ERR_STATE, "cdsgd_engine_check must run at least every 2^23 rounds");
