@@ -340,10 +340,12 @@ def small_layout_cold(args, dev, name="resnet20", n_sets=48, rounds=8):
                    f"state+inputs > 126 MB L2): each step starts from cold L2"}
 
 
-def fast_mode_rate(args, dev, layout, steps, warmup=8):
-    """The opt-in FAST mode on the same workload at N=1: fp32 residual (the fp32 restatement
-    of the quantizer, 12.25 instead of 20.25 B/elem) and fp32 weights. Not the reference's
-    arithmetic (the headline is the exact mode); reported beside it as SURVEY §8(b)/(c) ask."""
+def fast_mode_rate(args, dev, layout, steps, warmup=8, residual="f32"):
+    """The opt-in modes on the same workload at N=1, reported beside the exact headline:
+    residual="f32": the FAST mode — fp32 residual (the fp32 restatement of the quantizer,
+    12.25 instead of 20.25 B/elem) and fp32 weights, not the reference's arithmetic (SURVEY
+    §8(b)/(c)); residual="f64": fp32 weights only (round 1's arithmetic: bit-exact codes and
+    residuals, W rounded to fp32 every round)."""
     import torch
 
     from paper_2106_10796_b200.engine import HyperParams
@@ -353,7 +355,7 @@ def fast_mode_rate(args, dev, layout, steps, warmup=8):
     hp = HyperParams(algo="cdsgd", workers=1, eta_global=0.1, eta_local=0.4, k=args.k, alpha=args.alpha, warmup_n=0)
     gen = torch.Generator(device=dev).manual_seed(77)
     pool = [0.3 * torch.randn(n, device=dev, generator=gen) for _ in range(2)]
-    wk = CDSGDWorker(layout, hp, torch.zeros(n, device=dev), weights="f32", residual="f32")
+    wk = CDSGDWorker(layout, hp, torch.zeros(n, device=dev), weights="f32", residual=residual)
     for i in range(warmup):
         wk.step(pool[i % 2])
     torch.cuda.synchronize(dev)
@@ -372,11 +374,13 @@ def fast_mode_rate(args, dev, layout, steps, warmup=8):
     wk.close()
     nw = layout.n_words
     peak, _ = hbm_peak()
-    fb = 4 * n + 8 * n + 8 * n + 4 * n + 4 * nw + 4 * nw  # g | r r/w (fp32) | W r/w (fp32) | loc | codes in+out
+    rb = 4 if residual == "f32" else 8
+    fb = 4 * n + 2 * rb * n + 8 * n + 4 * n + 4 * nw + 4 * nw  # g | r r/w | W r/w (fp32) | loc | codes in+out
     f = prof["fused"]
-    out = {"residual": "fp32 (FAST mode: bitwise the fp32 restatement oracle, not the reference)",
-           "weights": "fp32", "value": n * steps / (ms / 1e3) / 1e9, "unit": UNIT, "ms_per_step": ms / steps,
-           "steps": steps}
+    out = {"residual": ("fp32 (FAST mode: bitwise the fp32 restatement oracle, not the reference)" if residual == "f32"
+                        else "fp64 (bit-exact)"),
+           "weights": "fp32 (rounded every round: drift envelope, DESIGN.md §3)",
+           "value": n * steps / (ms / 1e3) / 1e9, "unit": UNIT, "ms_per_step": ms / steps, "steps": steps}
     if f["n"]:
         us = 1e3 * f["ms"] / f["n"]
         out["fused"] = {"avg_us": us, "bytes_per_elem": fb / n, "achieved_gbs": fb / us / 1e3,
@@ -710,8 +714,9 @@ def run_ours(args):
     if world == 1 and args.workload == "resnet50" and not args.no_secondary:
         secondary = {"resnet20": small_layout_rate(args, dev)}
         secondary["resnet20"]["cold_l2"] = small_layout_cold(args, dev)
-        if args.residual == "f64":
-            secondary["fast_mode"] = fast_mode_rate(args, dev, layout, K)
+        if args.residual == "f64" and args.weights == "f64":
+            secondary["fp32_weights"] = fast_mode_rate(args, dev, layout, K, residual="f64")
+            secondary["fast_mode"] = fast_mode_rate(args, dev, layout, K, residual="f32")
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -596,6 +596,17 @@ int ch1_tiles_per_warp() {
     }();
     return v;
 }
+// Grid cap for chunk-task (small-layout) launches, in CTAs per SM (CDSGD_SMALL_CTAS_PER_SM;
+// default: no cap). Fewer CTAs leave slots for the next round's grid to become resident early
+// under programmatic dependent launch.
+int small_grid_cap() {
+    static const int v = [] {
+        const char* e = getenv("CDSGD_SMALL_CTAS_PER_SM");
+        const int c = e != nullptr ? atoi(e) : 0;
+        return c > 0 ? c * dev_info().sms : (1 << 30);
+    }();
+    return v;
+}
 template <int NR, int AP, typename TW, typename TR>
 int launch_fused_cfg(const FusedArgs& a, const KeyTab& kt, const DecodeTab& tab, cudaStream_t st) {
     constexpr int CHL = sizeof(TW) == 8 ? CDSGD_F64_CH : CHUNKS;  // chunks per task on large layouts
@@ -603,7 +614,8 @@ int launch_fused_cfg(const FusedArgs& a, const KeyTab& kt, const DecodeTab& tab,
     const int64_t warps =
         static_cast<int64_t>(resident_blocks(k_fused_ldg<NR, AP, CHL, TW, TR>, THREADS)) * WARPS_PER_BLOCK;
     if (kt.ntiles < ch1_tiles_per_warp() * warps)
-        launch_pdl(k_fused_ldg<NR, AP, 1, TW, TR>, tile_grid(k_fused_ldg<NR, AP, 1, TW, TR>, kt.ntiles * CHUNKS), THREADS,
+        launch_pdl(k_fused_ldg<NR, AP, 1, TW, TR>,
+                   std::min(tile_grid(k_fused_ldg<NR, AP, 1, TW, TR>, kt.ntiles * CHUNKS), small_grid_cap()), THREADS,
                    0, st, a, kt, tab);
     else
         launch_pdl(k_fused_ldg<NR, AP, CHL, TW, TR>,

@@ -1,7 +1,7 @@
 #!/bin/bash
 # small-layout (ResNet-20) A/B of env knobs + ncu launch list of the clean bench region
 mkdir -p gpurun_out
-for cfg in "default:" "ch1off:CDSGD_CH1_TPW=0" "ch1x8:CDSGD_CH1_TPW=8" "nopdl:CDSGD_NO_PDL=1" "static:CDSGD_STATIC_SCHED=1"; do
+for cfg in ${CFGS:-"default:" "cap1:CDSGD_SMALL_CTAS_PER_SM=1" "cap1s:CDSGD_SMALL_CTAS_PER_SM=1 CDSGD_STATIC_SCHED=1"}; do
   name=${cfg%%:*}; envs=${cfg#*:}
   env $envs timeout 300 python bench.py --workload resnet20 --steps 400 --warmup 20 --no-cpu-baseline --no-e2e --no-secondary --no-self-check > gpurun_out/${TAG}_$name.log 2>&1
   python - gpurun_out/${TAG}_$name.log $name <<'PY'
