@@ -680,6 +680,7 @@ extern "C" int cdsgd_fused_round(const cdsgd_layout* L, const float* grad, const
     if (L->n == 0) return CDSGD_OK;
     if (!grad || !r_in || !r_out || !words || !W || !loc) return fail(CDSGD_ERR_ARG, "NULL buffer");
     if (!wdt_ok(wdt)) return fail(CDSGD_ERR_ARG, "weights dtype must be CDSGD_F32 or CDSGD_F64");
+    if (!wdt_ok(r_dtype)) return fail(CDSGD_ERR_ARG, "residual dtype must be CDSGD_F32 or CDSGD_F64");
     FusedArgs a{};
     a.g = grad;
     a.r_in = r_in;
@@ -777,6 +778,12 @@ struct cdsgd_engine {
     const cdsgd_layout* L = nullptr;
     cdsgd_comm* comm = nullptr;
     cudaStream_t xs = nullptr, xs2 = nullptr;  // exchange streams (xs2: copy-engine share)
+    // one stream per peer for the copy-engine share's peer copies, so the N-1 transfers of a
+    // phase run on several copy engines at once instead of back to back on xs2
+    cudaStream_t xsc[MAX_RANKS_P2P] = {nullptr};
+    cudaEvent_t evc[MAX_RANKS_P2P] = {nullptr};
+    cudaEvent_t evfork = nullptr;
+    bool ce_parallel = false;          // CDSGD_CE_PARALLEL=1: one stream per peer copy
     cudaEvent_t evC = nullptr;
     cudaEvent_t evQ[2] = {nullptr, nullptr};
     cudaEvent_t evX[2] = {nullptr, nullptr};
@@ -960,6 +967,26 @@ void launch_reduce_w(const ReduceArgs& a, int64_t len, int wdt, cudaStream_t C) 
     else launch_reduce_t<NR, false, float>(a, len, C);
 }
 
+// Peer copies of one copy-engine phase: copy k (dst[k] <- src[k], bytes[k]) on stream xsc[k],
+// forked from and joined back into X, so the transfers to different peers overlap on several
+// copy engines (serially on X with CDSGD_CE_SERIAL=1).
+int ce_copies(cdsgd_engine* E, cudaStream_t X, int ncopy, void* const* dst, const void* const* src,
+              const size_t* bytes) {
+    if (!E->ce_parallel || ncopy <= 1) {
+        for (int k = 0; k < ncopy; ++k)
+            if (bytes[k]) CUDA_TRY(cudaMemcpyAsync(dst[k], src[k], bytes[k], cudaMemcpyDeviceToDevice, X));
+        return CDSGD_OK;
+    }
+    CUDA_TRY(cudaEventRecord(E->evfork, X));
+    for (int k = 0; k < ncopy; ++k) {
+        CUDA_TRY(cudaStreamWaitEvent(E->xsc[k], E->evfork, 0));
+        if (bytes[k]) CUDA_TRY(cudaMemcpyAsync(dst[k], src[k], bytes[k], cudaMemcpyDeviceToDevice, E->xsc[k]));
+        CUDA_TRY(cudaEventRecord(E->evc[k], E->xsc[k]));
+    }
+    for (int k = 0; k < ncopy; ++k) CUDA_TRY(cudaStreamWaitEvent(X, E->evc[k], 0));
+    return CDSGD_OK;
+}
+
 // Part of a correction round's all-reduce on the COPY ENGINES: elements [off, off + cnt)
 // of g_p. Each owner's slice goes to its receive row by cudaMemcpyAsync (no SMs), each
 // owner sums its shard from local rows (fp64, ascending rank, rounded once to fp32 — the
@@ -982,12 +1009,19 @@ int p2p_ce_allreduce(cdsgd_engine* E, int64_t p, const float* g, cudaStream_t X,
         k_wait_sum<<<1, 32, 0, X>>>(fw, nullptr, 0, nullptr, nullptr, nullptr);
         LAUNCH_CHECK();
     }
-    for (int k = 1; k < nr; ++k) {  // 2. reduce-scatter: my slice of owner o's shard -> o's row `me`
-        const int o = (me + k) % nr;   // (my own slice is read in place from g: no local copy)
-        const int64_t o0 = std::min<int64_t>(off + cnt, off + ck * o), o1 = std::min<int64_t>(off + cnt, o0 + ck);
-        if (o1 > o0)
-            CUDA_TRY(cudaMemcpyAsync(at<float>(E->peer[o], E->off_stage[s]) + static_cast<int64_t>(me) * ck, g + o0,
-                                     (o1 - o0) * sizeof(float), cudaMemcpyDeviceToDevice, X));
+    {  // 2. reduce-scatter: my slice of owner o's shard -> o's row `me` (my own slice is read in place)
+        void* dst[MAX_RANKS_P2P];
+        const void* src[MAX_RANKS_P2P];
+        size_t bytes[MAX_RANKS_P2P];
+        for (int k = 1; k < nr; ++k) {
+            const int o = (me + k) % nr;
+            const int64_t o0 = std::min<int64_t>(off + cnt, off + ck * o), o1 = std::min<int64_t>(off + cnt, o0 + ck);
+            dst[k - 1] = at<float>(E->peer[o], E->off_stage[s]) + static_cast<int64_t>(me) * ck;
+            src[k - 1] = g + o0;
+            bytes[k - 1] = o1 > o0 ? static_cast<size_t>(o1 - o0) * sizeof(float) : 0;
+        }
+        const int rc = ce_copies(E, X, nr - 1, dst, src, bytes);
+        if (rc != CDSGD_OK) return rc;
     }
     P2PArgs fr{};
     fr.nranks = nr;
@@ -1030,11 +1064,18 @@ int p2p_ce_allreduce(cdsgd_engine* E, int64_t p, const float* g, cudaStream_t X,
         k_flags<<<1, 32, 0, X>>>(a.xa);
         LAUNCH_CHECK();
     }
-    for (int k = 1; k < nr && m1 > m0; ++k) {  // 4. all-gather of my sum shard, then wdone[me]
-        const int r = (me + k) % nr;
-        CUDA_TRY(cudaMemcpyAsync(at<float>(E->peer[r], E->off_gsum[p & 1]) + m0,
-                                 at<const float>(local, E->off_gsum[p & 1]) + m0, (m1 - m0) * sizeof(float),
-                                 cudaMemcpyDeviceToDevice, X));
+    if (m1 > m0) {  // 4. all-gather of my sum shard, then wdone[me]
+        void* dst[MAX_RANKS_P2P];
+        const void* src[MAX_RANKS_P2P];
+        size_t bytes[MAX_RANKS_P2P];
+        for (int k = 1; k < nr; ++k) {
+            const int r = (me + k) % nr;
+            dst[k - 1] = at<float>(E->peer[r], E->off_gsum[p & 1]) + m0;
+            src[k - 1] = at<const float>(local, E->off_gsum[p & 1]) + m0;
+            bytes[k - 1] = static_cast<size_t>(m1 - m0) * sizeof(float);
+        }
+        const int rc = ce_copies(E, X, nr - 1, dst, src, bytes);
+        if (rc != CDSGD_OK) return rc;
     }
     P2PArgs fd{};
     fd.nranks = nr;
@@ -1261,6 +1302,15 @@ extern "C" int cdsgd_engine_create(const cdsgd_engine_desc* d, const cdsgd_layou
         e = cudaStreamCreateWithPriority(&E->xs, cudaStreamNonBlocking, hi);
         if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&E->xs2, cudaStreamNonBlocking, hi);
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(&E->evC, cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&E->evfork, cudaEventDisableTiming);
+        for (int i = 0; i < d->nranks && i < MAX_RANKS_P2P && e == cudaSuccess; ++i) {
+            e = cudaStreamCreateWithPriority(&E->xsc[i], cudaStreamNonBlocking, hi);
+            if (e == cudaSuccess) e = cudaEventCreateWithFlags(&E->evc[i], cudaEventDisableTiming);
+        }
+        // per-peer copy streams: measured no gain at N=4 (414 vs 420 Gelem/s serial; the copy
+        // engines' share takes as long either way) -> off by default, CDSGD_CE_PARALLEL=1 enables
+        const char* cs = getenv("CDSGD_CE_PARALLEL");
+        E->ce_parallel = cs != nullptr && cs[0] == '1';
         for (int i = 0; i < 2 && e == cudaSuccess; ++i) {
             e = cudaEventCreateWithFlags(&E->evQ[i], cudaEventDisableTiming);
             if (e == cudaSuccess) e = cudaEventCreateWithFlags(&E->evX[i], cudaEventDisableTiming);
@@ -1450,6 +1500,14 @@ extern "C" int cdsgd_engine_destroy(cdsgd_engine* E) {
     }
     if (E->xs) cudaStreamDestroy(E->xs);
     if (E->xs2) cudaStreamDestroy(E->xs2);
+    for (int i = 0; i < MAX_RANKS_P2P; ++i) {
+        if (E->xsc[i]) {
+            cudaStreamSynchronize(E->xsc[i]);
+            cudaStreamDestroy(E->xsc[i]);
+        }
+        if (E->evc[i]) cudaEventDestroy(E->evc[i]);
+    }
+    if (E->evfork) cudaEventDestroy(E->evfork);
     for (int i = 0; i < 4; ++i)
         if (E->win[i] != nullptr && E->comm != nullptr) ncclCommWindowDeregister(E->comm->nccl, E->win[i]);
     for (int i = 0; i < 2; ++i) {
