@@ -969,7 +969,7 @@ void launch_reduce_w(const ReduceArgs& a, int64_t len, int wdt, cudaStream_t C) 
 
 // Peer copies of one copy-engine phase: copy k (dst[k] <- src[k], bytes[k]) on stream xsc[k],
 // forked from and joined back into X, so the transfers to different peers overlap on several
-// copy engines (serially on X with CDSGD_CE_SERIAL=1).
+// copy engines (CDSGD_CE_PARALLEL=1; serially on X by default).
 int ce_copies(cdsgd_engine* E, cudaStream_t X, int ncopy, void* const* dst, const void* const* src,
               const size_t* bytes) {
     if (!E->ce_parallel || ncopy <= 1) {
