@@ -248,11 +248,13 @@ int launch_quant_tma_rdt(const float* g, int rdt, const void* r_in, void* r_out,
 }  // namespace
 
 // ------------------------------------------------------------------ layout
+constexpr int64_t MAX_TILE_TABLE = int64_t(1) << 17;  // tiles (64M elements): a 2 MB table
 struct cdsgd_layout {
     int32_t nkeys = 0;
     int64_t n = 0, nwords = 0, ntiles = 0;
     std::vector<int64_t> eoff, woff, toff;
     int64_t* dev = nullptr;  // [3 * (nkeys+1)]: eoff | woff | toff
+    int4* tiles = nullptr;   // [ntiles] per-tile metadata (layouts of <= MAX_TILE_TABLE tiles)
     int device = 0;
     KeyTab tab() const {
         KeyTab k;
@@ -261,6 +263,7 @@ struct cdsgd_layout {
         k.toff = dev + 2 * (nkeys + 1);
         k.nkeys = nkeys;
         k.ntiles = ntiles;
+        k.tiles = tiles;
         return k;
     }
 };
@@ -298,8 +301,26 @@ extern "C" int cdsgd_layout_create(const int64_t* lengths, int32_t n_keys, cdsgd
     h.insert(h.end(), L->toff.begin(), L->toff.end());
     cudaError_t e = cudaMalloc(&L->dev, h.size() * sizeof(int64_t));
     if (e == cudaSuccess) e = cudaMemcpy(L->dev, h.data(), h.size() * sizeof(int64_t), cudaMemcpyHostToDevice);
+    // per-tile table (16 B per 512 elements, capped at 2 MB; CDSGD_NO_TILE_TABLE=1 disables)
+    const char* nt = getenv("CDSGD_NO_TILE_TABLE");
+    if (e == cudaSuccess && L->ntiles <= MAX_TILE_TABLE && L->ntiles > 0 && !(nt != nullptr && nt[0] == '1') &&
+        L->nwords < (int64_t(1) << 31)) {
+        std::vector<int4> t(L->ntiles);
+        for (int32_t k = 0; k < n_keys; ++k)
+            for (int64_t ti = L->toff[k]; ti < L->toff[k + 1]; ++ti) {
+                const int64_t j = ti - L->toff[k];
+                const int64_t e0 = L->eoff[k] + j * TILE_ELEMS, w0 = L->woff[k] + j * TILE_WORDS;
+                const int64_t ne = std::min<int64_t>(TILE_ELEMS, L->eoff[k + 1] - e0);
+                const int64_t nw = std::min<int64_t>(TILE_WORDS, L->woff[k + 1] - w0);
+                t[ti] = make_int4(static_cast<int>(static_cast<uint32_t>(e0)), static_cast<int>(e0 >> 32),
+                                  static_cast<int>(w0), static_cast<int>(ne | (nw << 16)));
+            }
+        e = cudaMalloc(&L->tiles, t.size() * sizeof(int4));
+        if (e == cudaSuccess) e = cudaMemcpy(L->tiles, t.data(), t.size() * sizeof(int4), cudaMemcpyHostToDevice);
+    }
     if (e != cudaSuccess) {
         if (L->dev) cudaFree(L->dev);
+        if (L->tiles) cudaFree(L->tiles);
         delete L;
         return fail(CDSGD_ERR_CUDA, "layout upload: %s", cudaGetErrorString(e));
     }
@@ -310,6 +331,7 @@ extern "C" int cdsgd_layout_create(const int64_t* lengths, int32_t n_keys, cdsgd
 extern "C" int cdsgd_layout_destroy(cdsgd_layout* L) {
     if (L == nullptr) return CDSGD_OK;
     if (L->dev) cudaFree(L->dev);
+    if (L->tiles) cudaFree(L->tiles);
     delete L;
     return CDSGD_OK;
 }

@@ -36,6 +36,10 @@ struct KeyTab {
     const int64_t* toff;  // [nkeys+1] tile offsets
     int32_t nkeys;
     int64_t ntiles;
+    // Per-tile metadata {e0 lo, e0 hi, w0, ne | nw << 16} (nullptr for very large layouts):
+    // one 16-byte load locates a tile, instead of a key search (two dependent rounds of key-table
+    // loads) — on launch-bound layouts that search was a visible part of every round's latency.
+    const int4* tiles;
 };
 
 // ---------------------------------------------------------------- memory helpers
@@ -176,6 +180,18 @@ struct TileCursor {
     }
     __device__ __forceinline__ void advance_to(const KeyTab& kt, int64_t tile) {
         while (tile >= t1) load(kt, k + 1);
+    }
+    // Cursor over exactly tile `tile` from the per-tile table (kt.tiles != nullptr): t0 = tile,
+    // t1 = tile + 1, so the element / word ranges are the tile's own (the key index is unused).
+    __device__ __forceinline__ void from_table(const KeyTab& kt, int64_t tile) {
+        const int4 d = __ldg(kt.tiles + tile);
+        k = -1;
+        t0 = tile;
+        t1 = tile + 1;
+        e0 = (static_cast<int64_t>(static_cast<uint32_t>(d.y)) << 32) | static_cast<uint32_t>(d.x);
+        e1 = e0 + (d.w & 0xffff);
+        w0 = d.z;
+        w1 = w0 + (d.w >> 16);
     }
 };
 
@@ -703,7 +719,10 @@ __global__ void __launch_bounds__(WIDE ? 512 : 256, WIDE ? 1 : CDSGD_K2_MINB) k_
     }
     // constant inputs (tables, schedule, key seek) before griddepcontrol.wait (see k_fused_ldg)
     TileCursor kc;
-    if (tb < te) kc.seek_warp(kt, tb, lane);
+    if (tb < te) {
+        if (kt.tiles != nullptr) kc.from_table(kt, tb);
+        else kc.seek_warp(kt, tb, lane);
+    }
     pdl_enter(a.gclear[0], a.gclear[1]);
     const bool peer_failed = p2p_wait2(a.x, a.xs);
     const bool skip = peer_failed || (a.err != nullptr && *reinterpret_cast<volatile uint64_t*>(a.err) < a.skip_below);
@@ -719,7 +738,8 @@ __global__ void __launch_bounds__(WIDE ? 512 : 256, WIDE ? 1 : CDSGD_K2_MINB) k_
                 ti = nb;
                 cend = nb + (int64_t)cl < kt.ntiles ? nb + (int64_t)cl : kt.ntiles;
             }
-            kc.advance_warp(kt, ti, lane);
+            if (kt.tiles != nullptr) kc.from_table(kt, ti);
+            else kc.advance_warp(kt, ti, lane);
             const int64_t j = ti - kc.t0;
             const int64_t e0 = kc.e0 + j * TILE_ELEMS;
             const int64_t w0 = kc.w0 + j * TILE_WORDS;

@@ -228,7 +228,10 @@ __global__ void __launch_bounds__(256, sizeof(TW) == 8 ? CDSGD_F64_MINB : 2) k_f
         s_upd64[threadIdx.x] = tab.upd64[threadIdx.x];
     }
     TileCursor cc;
-    if (tb < te) cc.seek_warp(kt, tb / SPL, lane);
+    if (tb < te) {
+        if (kt.tiles != nullptr) cc.from_table(kt, tb / SPL);
+        else cc.seek_warp(kt, tb / SPL, lane);
+    }
     pdl_enter(a.gclear[0], a.gclear[1]);  // from here on: memory the preceding kernels write
     const bool peer_failed = p2p_wait2(a.xq, a.xa);
     const uint64_t e0v = a.err != nullptr ? *reinterpret_cast<volatile uint64_t*>(a.err) : ~0ull;
@@ -253,8 +256,12 @@ __global__ void __launch_bounds__(256, sizeof(TW) == 8 ? CDSGD_F64_MINB : 2) k_f
             }
             const int64_t ti = task / SPL;
             const int c0 = static_cast<int>(task % SPL) * CH;  // first chunk of this task
-            if (ti < cc.t0) cc.seek_warp(kt, ti, lane);
-            cc.advance_warp(kt, ti, lane);
+            if (kt.tiles != nullptr) {
+                if (ti != cc.t0) cc.from_table(kt, ti);
+            } else {
+                if (ti < cc.t0) cc.seek_warp(kt, ti, lane);
+                cc.advance_warp(kt, ti, lane);
+            }
             const int64_t j = ti - cc.t0;
             const int64_t e0 = cc.e0 + j * TILE_ELEMS;
             const int64_t w0 = cc.w0 + j * TILE_WORDS;
