@@ -851,6 +851,7 @@ struct cdsgd_engine {
     bool fuse = false;                 // apply(t-1) + quantize(t) in one kernel (N=1 or P2P)
     bool pcorr = false;                // P2P mode: correction rounds by the exact sharded NVLink reduce
     bool plain_after_ar = false;       // plain (non-PDL) launch of the apply beside a correction all-reduce
+    bool fuse_after_ar = false;        // N>1: quantize(t+1) fused with the correction's apply, after the all-reduce
     int reserve_sms = 0;               // SMs left free for the all-reduce's CTAs (CDSGD_RESERVE_SMS)
     // NCCL symmetric-window correction all-reduce (CDSGD_NCCL_SYM=1, p2p mode): g_t staged into an
     // ncclMemAlloc'ed, window-registered buffer (by K2, which streams g_t anyway), all-reduced into a
@@ -1304,6 +1305,8 @@ extern "C" int cdsgd_engine_create(const cdsgd_engine_desc* d, const cdsgd_layou
         E->fuse = d->nranks == 1 && !(nf != nullptr && nf[0] == '1');
         // A/B knob: plain launch of the apply beside a correction all-reduce (measured no gain at
         // N=2: 296 vs 301 Gelem/s — the apply's CTAs fill every SM either way)
+        const char* fa = getenv("CDSGD_FUSE_AFTER_AR");
+        E->fuse_after_ar = fa != nullptr && fa[0] == '1';
         const char* rs = getenv("CDSGD_RESERVE_SMS");
         E->reserve_sms = rs != nullptr ? std::max(0, atoi(rs)) : 0;
         const char* pa = getenv("CDSGD_PLAIN_AFTER_AR");
@@ -1627,7 +1630,13 @@ extern "C" int cdsgd_engine_step(cdsgd_engine* E, const float* g, void* stream) 
         E->t = t + 1;
         return CDSGD_OK;
     }
-    if (E->fuse && comp && !sync_path0 && (E->pending ? (E->pend_comp || nr == 1) : nr == 1)) {
+    // N>1, the round after a correction: apply the correction (its all-reduced sum) fused with
+    // this round's quantize, AFTER the all-reduce, instead of quantizing beside it and running
+    // K3 afterwards (CDSGD_FUSE_AFTER_AR; p2p exchange with the NCCL / copy-engine all-reduce)
+    const bool fuse_after_ar = E->fuse_after_ar && E->pending && !E->pend_comp && nr > 1 && E->p2p && !E->pcorr &&
+                               E->xused[E->pend_t & 1];
+    if (E->fuse && comp && !sync_path0 &&
+        (fuse_after_ar || (E->pending ? (E->pend_comp || nr == 1) : nr == 1))) {
         // ---- one kernel: apply(t-1) fused with quantize(t); both read g_t once. With nothing
         // pending (first local round, or N=1 after a folded correction) the apply part is just
         // loc_{t+1} = W_t - eta_l*g_t.
@@ -1644,7 +1653,9 @@ extern "C" int cdsgd_engine_step(cdsgd_engine* E, const float* g, void* stream) 
         a.loc = E->d.loc;
         a.gathered = E->d.gathered[pnd & 1];
         a.stride = nw;
-        a.gsum = E->pend_grad;  // N=1 correction round: the mean is g_{t-1} itself
+        // N=1 correction round: the mean is g_{t-1} itself; N>1: the all-reduced sum
+        a.gsum = fuse_after_ar ? E->d.gsum[pnd & 1] : E->pend_grad;
+        if (fuse_after_ar) CUDA_TRY(cudaStreamWaitEvent(C, E->evX[pnd & 1], 0));
         a.scale = static_cast<float>(E->d.eta_global / nr);
         a.inv_n = 1.0 / nr;
         a.eta_l = static_cast<float>(E->d.eta_local);
@@ -1686,7 +1697,7 @@ extern "C" int cdsgd_engine_step(cdsgd_engine* E, const float* g, void* stream) 
             a.xa.sc_fence = E->sc_fence;
             a.xa.err = E->d.err;
             if (E->diag_no_wait) a.xq.wait_value = a.xa.wait_value = 0;
-            if (!has_pend) a.xa.nranks = 0;  // nothing to consume (local-only pass)
+            if (!has_pend || fuse_after_ar) a.xa.nranks = 0;  // no codes to consume (local-only / full apply)
             E->last_use[p] = t;
         }
         E->rlog.push_back(static_cast<int8_t>(E->rcur));
