@@ -185,6 +185,9 @@ __global__ void __launch_bounds__(256) k_reduce(ReduceArgs a) {
     }
 }
 
+// Empty kernel: a stream-ordered marker (CDSGD_AR_FIRST gate before the correction all-reduce).
+__global__ void k_noop() {}
+
 // One thread: release publish_value to every rank's flag cell after everything earlier on
 // this stream (copy-engine transfers included) has completed.
 __global__ void k_flags(P2PArgs x) {
