@@ -853,7 +853,18 @@ struct cdsgd_engine {
     bool plain_after_ar = false;       // plain (non-PDL) launch of the apply beside a correction all-reduce
     bool fuse_after_ar = false;        // N>1: quantize(t+1) fused with the correction's apply, after the all-reduce
     bool ar_first = true;              // gate the apply behind a marker on the exchange stream (CDSGD_AR_FIRST)
+    // Copy-engine share, second half deferred to the next step (CDSGD_CE_DEFER, default on): the
+    // shard reduce runs on C right after the apply of the correction step (all SMs but NCCL's,
+    // instead of starving beside it), and the all-gather on the copy engines overlaps K1.
+    bool ce_defer = true;
+    struct CePending {
+        bool on = false;
+        int64_t p = 0, off = 0, cnt = 0, ck = 0, m0 = 0, m1 = 0;
+        int s = 0;
+        const float* g = nullptr;
+    } ce_pend;
     cudaEvent_t evG = nullptr;
+    cudaEvent_t evR = nullptr;         // the deferred copy-engine reduce is done (on C)
     int reserve_sms = 0;               // SMs left free for the all-reduce's CTAs (CDSGD_RESERVE_SMS)
     // NCCL symmetric-window correction all-reduce (CDSGD_NCCL_SYM=1, p2p mode): g_t staged into an
     // ncclMemAlloc'ed, window-registered buffer (by K2, which streams g_t anyway), all-reduced into a
@@ -992,6 +1003,24 @@ void launch_reduce_w(const ReduceArgs& a, int64_t len, int wdt, cudaStream_t C) 
     else launch_reduce_t<NR, false, float>(a, len, C);
 }
 
+int p2p_ce_reduce_gather(cdsgd_engine* E, int64_t p, const float* g, cudaStream_t R, cudaStream_t X, int s,
+                         int64_t ck, int64_t m0, int64_t m1);
+
+// Issue the deferred second half of a correction's copy-engine share: the reduce on C (this
+// step's stream, before anything else of the step), the all-gather on xs2; then the correction's
+// completion event evX on xs joins NCCL's share (xs) and the copy-engine share (xs2).
+int p2p_ce_finish(cdsgd_engine* E, cudaStream_t C) {
+    if (!E->ce_pend.on) return CDSGD_OK;
+    const auto cp = E->ce_pend;
+    E->ce_pend.on = false;
+    const int rc = p2p_ce_reduce_gather(E, cp.p, cp.g, C, E->xs2, cp.s, cp.ck, cp.m0, cp.m1);
+    if (rc != CDSGD_OK) return rc;
+    CUDA_TRY(cudaEventRecord(E->evC, E->xs2));
+    CUDA_TRY(cudaStreamWaitEvent(E->xs, E->evC, 0));
+    CUDA_TRY(cudaEventRecord(E->evX[cp.p & 1], E->xs));
+    return CDSGD_OK;
+}
+
 // Peer copies of one copy-engine phase: copy k (dst[k] <- src[k], bytes[k]) on stream xsc[k],
 // forked from and joined back into X, so the transfers to different peers overlap on several
 // copy engines (CDSGD_CE_PARALLEL=1; serially on X by default).
@@ -1054,6 +1083,27 @@ int p2p_ce_allreduce(cdsgd_engine* E, int64_t p, const float* g, cudaStream_t X,
     fr.publish_value = static_cast<uint64_t>(p) + 1;
     k_flags<<<1, 32, 0, X>>>(fr);
     LAUNCH_CHECK();
+    if (E->ce_defer) {  // steps 3-5 are issued by the next step (p2p_ce_finish)
+        E->ce_pend.on = true;
+        E->ce_pend.p = p;
+        E->ce_pend.off = off;
+        E->ce_pend.cnt = cnt;
+        E->ce_pend.ck = ck;
+        E->ce_pend.m0 = m0;
+        E->ce_pend.m1 = m1;
+        E->ce_pend.s = s;
+        E->ce_pend.g = g;
+        return CDSGD_OK;
+    }
+    return p2p_ce_reduce_gather(E, p, g, X, X, s, ck, m0, m1);
+}
+
+// Steps 3-5 of the copy-engine share: the shard reduce (a kernel) on stream R, the all-gather
+// copies, flags and the completion wait on stream X.
+int p2p_ce_reduce_gather(cdsgd_engine* E, int64_t p, const float* g, cudaStream_t R, cudaStream_t X, int s,
+                         int64_t ck, int64_t m0, int64_t m1) {
+    const int nr = E->d.nranks, me = E->d.rank;
+    char* local = E->peer[me];
     ReduceArgs a{};  // 3. my shard from the N local rows -> my gsum (fp32 of the fp64 sum)
     for (int r = 0; r < nr; ++r) {
         a.stage[r] = r == me ? g : at<const float>(local, E->off_stage[s]) + static_cast<int64_t>(r) * ck - m0;
@@ -1073,21 +1123,25 @@ int p2p_ce_allreduce(cdsgd_engine* E, int64_t p, const float* g, cudaStream_t X,
     a.xa.err = E->d.err;
     if (m1 > m0) {
         switch (nr) {
-            case 2: launch_reduce_t<2, true>(a, m1 - m0, X); break;
-            case 3: launch_reduce_t<3, true>(a, m1 - m0, X); break;
-            case 4: launch_reduce_t<4, true>(a, m1 - m0, X); break;
-            case 5: launch_reduce_t<5, true>(a, m1 - m0, X); break;
-            case 6: launch_reduce_t<6, true>(a, m1 - m0, X); break;
-            case 7: launch_reduce_t<7, true>(a, m1 - m0, X); break;
-            case 8: launch_reduce_t<8, true>(a, m1 - m0, X); break;
+            case 2: launch_reduce_t<2, true>(a, m1 - m0, R); break;
+            case 3: launch_reduce_t<3, true>(a, m1 - m0, R); break;
+            case 4: launch_reduce_t<4, true>(a, m1 - m0, R); break;
+            case 5: launch_reduce_t<5, true>(a, m1 - m0, R); break;
+            case 6: launch_reduce_t<6, true>(a, m1 - m0, R); break;
+            case 7: launch_reduce_t<7, true>(a, m1 - m0, R); break;
+            case 8: launch_reduce_t<8, true>(a, m1 - m0, R); break;
             default: return fail(CDSGD_ERR_ARG, "P2P correction supports 2..8 ranks");
         }
         LAUNCH_CHECK();
     } else {  // empty shard: still take part in the ready / freed protocol
-        k_wait_sum<<<1, 32, 0, X>>>(a.xa, nullptr, 0, nullptr, nullptr, nullptr);
+        k_wait_sum<<<1, 32, 0, R>>>(a.xa, nullptr, 0, nullptr, nullptr, nullptr);
         LAUNCH_CHECK();
-        k_flags<<<1, 32, 0, X>>>(a.xa);
+        k_flags<<<1, 32, 0, R>>>(a.xa);
         LAUNCH_CHECK();
+    }
+    if (R != X) {  // the all-gather (copy engines) after the reduce, on the exchange stream
+        CUDA_TRY(cudaEventRecord(E->evR, R));
+        CUDA_TRY(cudaStreamWaitEvent(X, E->evR, 0));
     }
     if (m1 > m0) {  // 4. all-gather of my sum shard, then wdone[me]
         void* dst[MAX_RANKS_P2P];
@@ -1311,6 +1365,8 @@ extern "C" int cdsgd_engine_create(const cdsgd_engine_desc* d, const cdsgd_layou
         // them all: a marker kernel on the exchange stream gates the apply, so NCCL's kernel is
         // eligible first and overlaps K2 (it used to start only when K2 retired). Measured
         // +2.5 % at N=2, +5-7 % at N=4 (436 vs 413 Gelem/s). CDSGD_AR_FIRST=0 disables.
+        const char* cd = getenv("CDSGD_CE_DEFER");
+        E->ce_defer = !(cd != nullptr && cd[0] == '0');
         const char* af = getenv("CDSGD_AR_FIRST");
         E->ar_first = !(af != nullptr && af[0] == '0');
         const char* fa = getenv("CDSGD_FUSE_AFTER_AR");
@@ -1337,6 +1393,7 @@ extern "C" int cdsgd_engine_create(const cdsgd_engine_desc* d, const cdsgd_layou
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(&E->evC, cudaEventDisableTiming);
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(&E->evfork, cudaEventDisableTiming);
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(&E->evG, cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&E->evR, cudaEventDisableTiming);
         for (int i = 0; i < d->nranks && i < MAX_RANKS_P2P && e == cudaSuccess; ++i) {
             e = cudaStreamCreateWithPriority(&E->xsc[i], cudaStreamNonBlocking, hi);
             if (e == cudaSuccess) e = cudaEventCreateWithFlags(&E->evc[i], cudaEventDisableTiming);
@@ -1492,6 +1549,8 @@ extern "C" int cdsgd_engine_attach_p2p(cdsgd_engine* E, void* const* peer_bases,
 
 extern "C" int cdsgd_engine_join(cdsgd_engine* E, void* stream) {
     if (E == nullptr) return fail(CDSGD_ERR_ARG, "NULL engine");
+    const int rf = p2p_ce_finish(E, S(stream));  // a deferred copy-engine half is part of "issued"
+    if (rf != CDSGD_OK) return rf;
     if (E->xs == nullptr || E->t == 0) return CDSGD_OK;
     for (int64_t u = E->t - 1; u >= 0 && u >= E->t - 2; --u)
         if (E->xused[u & 1]) CUDA_TRY(cudaStreamWaitEvent(S(stream), E->evX[u & 1], 0));
@@ -1543,6 +1602,7 @@ extern "C" int cdsgd_engine_destroy(cdsgd_engine* E) {
     }
     if (E->evfork) cudaEventDestroy(E->evfork);
     if (E->evG) cudaEventDestroy(E->evG);
+    if (E->evR) cudaEventDestroy(E->evR);
     for (int i = 0; i < 4; ++i)
         if (E->win[i] != nullptr && E->comm != nullptr) ncclCommWindowDeregister(E->comm->nccl, E->win[i]);
     for (int i = 0; i < 2; ++i) {
@@ -1582,7 +1642,9 @@ extern "C" int cdsgd_engine_step(cdsgd_engine* E, const float* g, void* stream) 
     cudaStream_t C = S(stream);
     const int64_t t = E->t;
     bool comp = false;
-    int rc = round_compressed(E, t, &comp);
+    int rc = p2p_ce_finish(E, C);  // the previous correction's deferred copy-engine reduce + all-gather
+    if (rc != CDSGD_OK) return rc;
+    rc = round_compressed(E, t, &comp);
     if (rc != CDSGD_OK) return rc;
     const int nr = E->d.nranks;
     const int64_t nw = words_of(E);
@@ -1799,9 +1861,11 @@ extern "C" int cdsgd_engine_step(cdsgd_engine* E, const float* g, void* stream) 
         rc = p2p_ce_allreduce(E, t, g, E->xs2, off, cnt);
         if (rc != CDSGD_OK) return rc;
         prof_stop(E, pc, E->xs2);
-        CUDA_TRY(cudaEventRecord(E->evC, E->xs2));
-        CUDA_TRY(cudaStreamWaitEvent(E->xs, E->evC, 0));
-        CUDA_TRY(cudaEventRecord(E->evX[t & 1], E->xs));
+        if (!E->ce_pend.on) {  // (deferred: the next step's p2p_ce_finish records evX)
+            CUDA_TRY(cudaEventRecord(E->evC, E->xs2));
+            CUDA_TRY(cudaStreamWaitEvent(E->xs, E->evC, 0));
+            CUDA_TRY(cudaEventRecord(E->evX[t & 1], E->xs));
+        }
     } else if (E->xused[t & 1] && !comp && E->nccl_sym) {
         // deferred until after the apply below, which stages g_t into the registered buffer
     } else if (E->xused[t & 1]) {
@@ -1901,6 +1965,8 @@ extern "C" int cdsgd_engine_step(cdsgd_engine* E, const float* g, void* stream) 
 
 extern "C" int cdsgd_engine_flush(cdsgd_engine* E, void* stream) {
     if (E == nullptr) return fail(CDSGD_ERR_ARG, "NULL engine");
+    const int rf = p2p_ce_finish(E, S(stream));
+    if (rf != CDSGD_OK) return rf;
     if (!E->pending) return CDSGD_OK;
     const int rc = engine_apply(E, E->pend_t, E->pend_comp, E->pend_grad, nullptr, S(stream));
     if (rc != CDSGD_OK) return rc;
