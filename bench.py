@@ -151,6 +151,13 @@ def ncu_traffic(workload: str, kernel: str):
 # ----------------------------------------------------------------------------- CPU legs
 
 
+def host_threads() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
 def python_reference(layout, args, n_workers, budget_s=40.0):
     """The UNMODIFIED reference (baseline/_ref, pure Python/NumPy, 1 core) on the same host:
     its lock-step step loop on the full workload layout for a few rounds, on BASELINE
@@ -178,9 +185,10 @@ def cpu_baseline(layout, args, n_workers):
     sample), whole k-periods, ~args.cpu_seconds; beside it the unmodified Python reference."""
     from oracle import cpu_port, ref_python
 
-    tk, kind, cores, impl = cpu_port.time_rounds(layout.lengths, n_workers, args.k, args.alpha, args.k)
+    th = host_threads()
+    tk, kind, cores, impl = cpu_port.time_rounds(layout.lengths, n_workers, args.k, args.alpha, args.k, threads=th)
     rounds = max(args.k, int(args.cpu_seconds / max(tk / args.k, 1e-6)) // args.k * args.k)
-    secs, kind, cores, impl = cpu_port.time_rounds(layout.lengths, n_workers, args.k, args.alpha, rounds)
+    secs, kind, cores, impl = cpu_port.time_rounds(layout.lengths, n_workers, args.k, args.alpha, rounds, threads=th)
     value = n_workers * layout.total * rounds / secs / 1e9
     return {"value": value, "unit": UNIT, "cores": cores, "kind": kind,
             "sample": f"{rounds} lock-step rounds x {n_workers} worker(s) on the FULL {args.workload} layout "
@@ -203,8 +211,10 @@ def run_reference(args):
 
     layout = by_name(args.workload)
     n_workers = max(args.gpus, world)
+    # all host threads: torchrun exports OMP_NUM_THREADS=1 to every rank, which would pin the
+    # OpenMP C port to one core
     secs, kind, cores, impl = cpu_port.time_rounds(layout.lengths, n_workers, args.k, args.alpha, args.steps,
-                                                   warm=max(1, args.warmup))
+                                                   warm=max(1, args.warmup), threads=host_threads())
     value = n_workers * layout.total * args.steps / secs / 1e9
     desc = (f"{args.steps} lock-step rounds x {n_workers} simulated workers on the FULL {args.workload} layout "
             f"({len(layout)} keys, {layout.total:,} elements), after {max(1, args.warmup)} untimed; {impl}")
