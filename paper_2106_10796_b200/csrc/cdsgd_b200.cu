@@ -271,6 +271,15 @@ struct cdsgd_layout {
 extern "C" int cdsgd_abi_version(void) { return CDSGD_ABI_VERSION; }
 extern "C" const char* cdsgd_last_error(void) { return g_err; }
 extern "C" uint64_t cdsgd_launch_count(void) { return g_launches.load(); }
+#ifdef CDSGD_PROBE_TIMING
+// development builds only: the fused kernel's per-warp phase stamps of its last launch
+extern "C" int cdsgd_diag_probe(unsigned long long* host, int64_t n) {
+    const int64_t cap = static_cast<int64_t>(cdsgd::PROBE_WARPS) * cdsgd::PROBE_PTS;
+    if (cudaMemcpyFromSymbol(host, cdsgd::g_probe, sizeof(unsigned long long) * (n < cap ? n : cap)) != cudaSuccess)
+        return CDSGD_ERR_CUDA;
+    return CDSGD_OK;
+}
+#endif
 
 extern "C" int cdsgd_layout_create(const int64_t* lengths, int32_t n_keys, cdsgd_layout** out) {
     if (out == nullptr) return fail(CDSGD_ERR_ARG, "out is NULL");

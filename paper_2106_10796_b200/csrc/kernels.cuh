@@ -198,12 +198,16 @@ struct TileCursor {
 __device__ __forceinline__ void warp_range(int64_t ntiles, int64_t& b, int64_t& e) {
     const int64_t wid = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
-    const int64_t per = (ntiles + nw - 1) / nw;
+    // one task per warp or fewer (launch-bound layouts): no 64-bit division in the prologue
+    const int64_t per = ntiles <= nw ? 1 : (ntiles + nw - 1) / nw;
     b = wid * per;
     e = b + per < ntiles ? b + per : ntiles;
 }
 
 __device__ __forceinline__ uint64_t warp_min_u64(uint64_t v) {
+    // error indices are the exception: one vote skips the 10-shuffle chain (it sat on every
+    // warp's exit path, a visible share of a launch-bound round)
+    if (!__any_sync(FULL, v != ~0ull)) return ~0ull;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         uint64_t u = __shfl_xor_sync(FULL, v, o);
@@ -227,6 +231,38 @@ __device__ __forceinline__ void block_atomic_add(double v, double* dst) {
         double t = (threadIdx.x < nwarp) ? s_part[threadIdx.x] : 0.0;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(FULL, t, o);
+        if (threadIdx.x == 0 && t != 0.0) atomicAdd(dst, t);
+    }
+}
+// The same for a grad-norm partial given as an integer count sum (the exact decode table:
+// sum of cnt^2, times sq_scale = (alpha/N)^2) plus a double part that is zero on that path:
+// the integer goes through one redux.sync per warp instead of a dependent chain of ten
+// 64-bit shuffles + adds, and the double chain runs only in warps that hold a nonzero part.
+// The CTA's value is gsq + isq * sq_scale with the integer summed exactly first.
+__device__ __forceinline__ void block_atomic_add_counts(int isq, double gsq, double sq_scale, double* dst) {
+    __shared__ double s_dpart[32];
+    __shared__ unsigned s_ipart[32];
+    const unsigned wi = __reduce_add_sync(FULL, static_cast<unsigned>(isq));
+    if (__any_sync(FULL, gsq != 0.0)) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) gsq += __shfl_xor_sync(FULL, gsq, o);
+    }
+    const int warp = threadIdx.x >> 5, nwarp = (blockDim.x + 31) >> 5;
+    __syncthreads();  // the parts may still be read by a previous call
+    if ((threadIdx.x & 31) == 0) {
+        s_ipart[warp] = wi;
+        s_dpart[warp] = gsq;
+    }
+    __syncthreads();
+    if (warp == 0) {
+        double t = (threadIdx.x < nwarp) ? s_dpart[threadIdx.x] : 0.0;
+        if (__any_sync(FULL, t != 0.0)) {
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(FULL, t, o);
+        }
+        uint64_t ti = 0;  // 64-bit CTA total (per-warp sums are 32-bit)
+        for (int w = 0; w < nwarp; ++w) ti += s_ipart[w];
+        t += static_cast<double>(ti) * sq_scale;
         if (threadIdx.x == 0 && t != 0.0) atomicAdd(dst, t);
     }
 }
@@ -371,8 +407,13 @@ __device__ __forceinline__ void p2p_publish(const P2PArgs& x) {
 }
 
 // One barrier for both waits (each waits only if armed); true if a peer is poisoned.
+__device__ __forceinline__ bool p2p_has_wait(const P2PArgs& x) {
+    return x.nranks > 0 && x.wait_flags != nullptr && x.wait_value != 0;
+}
 __device__ __forceinline__ bool p2p_wait2(const P2PArgs& a, const P2PArgs& b) {
     __shared__ int s_poison2;
+    // nothing to wait for (N = 1, local codes): no barrier on the launch's critical path
+    if (!p2p_has_wait(a) && !p2p_has_wait(b)) return false;
     if (threadIdx.x == 0) {
         const long long t0 = clock64();
         const bool pa = p2p_wait_t0(a, t0);
@@ -488,6 +529,11 @@ struct DecodeTab {
 // the round mean is exact (N = 1); the compute weights loc = fl32(W - eta_l*g) are the
 // reference's fp64 local update (engine.py:268-274) rounded once to fp32. In fp32 W is
 // rounded once per round (a random-walk drift).
+// Compiler barrier on a value: it must be materialised here (keeps a load from being sunk
+// into a later conditional block); no instruction is emitted.
+__device__ __forceinline__ void pin(float& x) { asm volatile("" : "+f"(x)); }
+__device__ __forceinline__ void pin(double& x) { asm volatile("" : "+d"(x)); }
+
 template <typename TW> struct WV;  // 4 consecutive weights of one lane
 template <> struct WV<float> { float v[4]; };
 template <> struct WV<double> { double v[4]; };
@@ -805,7 +851,7 @@ __global__ void __launch_bounds__(WIDE ? 512 : 256, WIDE ? 1 : CDSGD_K2_MINB) k_
             }
         }
     }
-    if (a.gnorm != nullptr) block_atomic_add(gsq + static_cast<double>(isq) * tab.sq_scale, a.gnorm);
+    if (a.gnorm != nullptr) block_atomic_add_counts(isq, gsq, tab.sq_scale, a.gnorm);
     if (a.gnorm2 != nullptr) block_atomic_add(gsq2, a.gnorm2);
     if (a.err != nullptr) {
         bad_idx = warp_min_u64(bad_idx);

@@ -1,16 +1,25 @@
 #!/bin/bash
-# small-layout (ResNet-20) A/B of env knobs + ncu launch list of the clean bench region
+# small-layout latency probe: knob variants, then one ncu --set full of the ResNet-20 fused kernel
 mkdir -p gpurun_out
-for cfg in ${CFGS:-"default:" "cap1:CDSGD_SMALL_CTAS_PER_SM=1" "cap1s:CDSGD_SMALL_CTAS_PER_SM=1 CDSGD_STATIC_SCHED=1"}; do
-  name=${cfg%%:*}; envs=${cfg#*:}
-  env $envs timeout 300 python bench.py --workload resnet20 --steps 400 --warmup 20 --no-cpu-baseline --no-e2e --no-secondary --no-self-check > gpurun_out/${TAG}_$name.log 2>&1
-  python - gpurun_out/${TAG}_$name.log $name <<'PY'
-import json,sys
-l=[x for x in open(sys.argv[1]) if x.startswith("{")]
-if not l: print(sys.argv[2], open(sys.argv[1]).read()[-600:]); sys.exit()
-d=json.loads(l[-1]); print(sys.argv[2], "value", round(d["value"],1), "us/step", round(d["ms_per_step"]*1e3,2), " ".join(f"{k}:{v['avg_us']:.1f}" for k,v in d["kernels"].items()))
+O=gpurun_out/${TAG}_small.jsonl; : > $O
+P="python scripts/small_probe.py --periods 1,10"
+timeout 300 $P --floor --tag default >> $O 2>gpurun_out/${TAG}_small.err
+CDSGD_NO_PDL=1 timeout 300 $P --tag nopdl >> $O 2>>gpurun_out/${TAG}_small.err
+CDSGD_SMALL_CTAS_PER_SM=1 timeout 300 $P --tag cap1 >> $O 2>>gpurun_out/${TAG}_small.err
+CDSGD_CH1_TPW=0 timeout 300 $P --tag noch1 >> $O 2>>gpurun_out/${TAG}_small.err
+CDSGD_NO_TILE_TABLE=1 timeout 300 $P --tag notab >> $O 2>>gpurun_out/${TAG}_small.err
+timeout 300 $P --weights f32 --tag f32w >> $O 2>>gpurun_out/${TAG}_small.err
+timeout 300 python scripts/small_probe.py --layout single:262144 --periods 10 --tag s2p18 >> $O 2>>gpurun_out/${TAG}_small.err
+python - <<PY
+import json
+for l in open("$O"):
+    d=json.loads(l); print(d["tag"], {k:round(v,2) for k,v in d["us_per_step"].items()}, round(d["best_gelem_s"],1), d.get("us_per_tiny_kernel_in_graph"))
 PY
+timeout 600 ncu --set full --import-source on --clock-control none -k regex:k_fused -s 40 -c 4 -o gpurun_out/${TAG}_r20 python scripts/small_probe.py --periods 10 --reps 10 > gpurun_out/${TAG}_ncu.log 2>&1; echo "ncu rc=$?"
+for f in gpurun_out/${TAG}_r20.ncu-rep; do
+  ncu -i $f --page raw --csv > gpurun_out/${TAG}_r20_raw.csv 2>/dev/null
+  ncu -i $f --page details > gpurun_out/${TAG}_r20_details.txt 2>/dev/null
+  ncu -i $f --page source --csv > gpurun_out/${TAG}_r20_source.csv 2>/dev/null
+  rm -f $f
 done
-timeout 300 python bench.py --workload resnet20 --steps 8 --warmup 4 --no-cpu-baseline --no-e2e --no-secondary --no-self-check > gpurun_out/${TAG}_plain.log 2>&1 && \
-timeout 300 ncu --metrics gpu__time_duration.sum,launch__grid_size,launch__registers_per_thread --clock-control none -k regex:cdsgd -c 40 --csv --log-file gpurun_out/${TAG}_launches.csv python bench.py --workload resnet20 --steps 8 --warmup 4 --no-cpu-baseline --no-e2e --no-secondary --no-self-check > gpurun_out/${TAG}_ncu.log 2>&1
-echo "ncu rc=$?"
+ls -la gpurun_out/${TAG}_*
