@@ -503,6 +503,8 @@ void build_tab(DecodeTab& tab, double alpha, double eta_g, int nr) {
 }
 inline bool pow2(int n) { return n > 0 && (n & (n - 1)) == 0; }
 
+int ch1_tiles_per_warp();
+int small_grid_cap();
 int launch_apply_quant(const cdsgd_layout* L, void* W, int wdt, const uint32_t* gathered, int nr, int64_t stride,
                        double alpha, double eta_g, const float* gnext, float* loc, double eta_l, uint64_t* err,
                        uint64_t skip_below, double* gnorm, const DecodeTab* tab_in, int exact_in,
@@ -562,10 +564,18 @@ int launch_apply_quant(const cdsgd_layout* L, void* W, int wdt, const uint32_t* 
         LAUNCH_CHECK();
         return CDSGD_OK;
     }
+    // small layouts (fewer than ~2 whole tiles per resident warp): one 128-element chunk per
+    // warp task, as the fused kernel (4x the warps in flight)
 #define AQ(R, TW)                                                                                       \
     case R:                                                                                             \
-        launch_pdl(k_apply_quant<R, 0, TW>, tile_grid(k_apply_quant<R, 0, TW>, kt.ntiles), THREADS, 0, st, a, kt, \
-                   tab);                                                                                \
+        if (kt.ntiles < ch1_tiles_per_warp() * static_cast<int64_t>(resident_blocks(k_apply_quant<R, 0, TW>, THREADS)) * \
+                            WARPS_PER_BLOCK)                                                            \
+            launch_pdl(k_apply_quant<R, 0, TW, 1>,                                                      \
+                       std::min(tile_grid(k_apply_quant<R, 0, TW, 1>, kt.ntiles * CHUNKS), small_grid_cap()), THREADS, \
+                       0, st, a, kt, tab);                                                              \
+        else                                                                                            \
+            launch_pdl(k_apply_quant<R, 0, TW>, tile_grid(k_apply_quant<R, 0, TW>, kt.ntiles), THREADS, 0, st, a, kt, \
+                       tab);                                                                            \
         break
     if (wdt == CDSGD_F64) {
         switch (nr) {

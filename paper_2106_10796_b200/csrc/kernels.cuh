@@ -662,33 +662,77 @@ __device__ __forceinline__ double apply_mean_general(const uint32_t* codes, int 
     return inv_n != 0.0 ? __dmul_rn(tot, inv_n) : __ddiv_rn(tot, static_cast<double>(nr));
 }
 
-// K2 vector path for one tile (exact-alpha table, compile-time rank count). Tiles of ne <
-// TILE_ELEMS elements (a key's last) use masked accesses; padding codes are ignored.
-template <int NR, typename TW, bool FULL>  // FULL: whole tile, unmasked accesses (see fused_vec_task)
-__device__ __forceinline__ void apply_vec_tile(const ApplyQArgs& a, const float* s_upd, const double* s_upd64, int nr,
-                                               int lane, int64_t e0, int64_t w0, int ne, int nw, bool do_loc, int so0,
-                                               int64_t sbnd, int& isq, double& gsq2, uint64_t& bad_idx) {
-    constexpr int R = NR > 0 ? NR : 1;
-    TW* const W = static_cast<TW*>(a.W);
-    uint32_t wv[R];
-#pragma unroll
-    for (int r = 0; r < R; ++r) wv[r] = lane < nw ? ld_word(a.gathered + r * a.stride + w0 + lane) : 0u;
-    WV<TW> wt[CHUNKS];
-    float4 gt[CHUNKS];
-#pragma unroll
-    for (int c = 0; c < CHUNKS; ++c) {
-        const int64_t e = e0 + 128 * c + 4 * lane;
-        const int nv = FULL ? 4 : nvalid4(ne, 128 * c + 4 * lane);
-        ldw4(W + e, nv, wt[c]);
-        if (do_loc) gt[c] = ld_stream_m(a.gnext + e, nv);
+// Write-only scratch for the stores of an aborted round on the branch-free small-layout
+// paths (32 lanes x 32 bytes; concurrent garbage writes from every warp are harmless).
+__device__ __align__(32) double g_sink[32 * 4];
+template <typename T>
+__device__ __forceinline__ T* sink_of(double* sink, int lane) {
+    return reinterpret_cast<T*>(sink + 4 * lane);
+}
+
+// K2's operands of one task (registers), see apply_vec_load.
+template <int NR, typename TW, int CH>
+struct K2Regs {
+    uint32_t wv[NR > 0 ? NR : 1];
+    WV<TW> wt[CH];
+    float4 gt[CH];
+};
+// K2 pointers held in registers from before the grid-dependency wait on small layouts
+// (see HotPtrs in kernels_fused.cuh: parameter reloads after the wait were on every warp's
+// path to its loads).
+struct K2Hot {
+    void* W;
+    const uint32_t* gathered;
+    const float* gnext;
+    float* loc;
+    double* sink;
+    int p2p_wait;
+    __device__ __forceinline__ explicit K2Hot(const ApplyQArgs& a)
+        : W(a.W), gathered(a.gathered), gnext(a.gnext), loc(a.loc), sink(g_sink),
+          p2p_wait(p2p_has_wait(a.x) || p2p_has_wait(a.xs) ? 1 : 0) {}
+    __device__ __forceinline__ void pin_here() {
+        asm volatile("" : "+l"(W), "+l"(gathered), "+l"(gnext), "+l"(loc), "+l"(sink), "+r"(p2p_wait));
     }
+};
+
+// K2 vector path for one task: CH chunks of 128 elements (from chunk c0) of a tile (exact-alpha
+// table, compile-time rank count). Tiles of ne < TILE_ELEMS elements (a key's last) use masked
+// accesses; padding codes are ignored.
+template <int NR, typename TW, bool FULL, int CH>  // FULL: whole tile, unmasked accesses (see fused_vec_task)
+__device__ __forceinline__ void apply_vec_load(const ApplyQArgs& a, const K2Hot& h, int lane, int64_t e0, int64_t w0,
+                                               int ne, int nw, int c0, bool do_loc, K2Regs<NR, TW, CH>& L) {
+    constexpr int R = NR > 0 ? NR : 1;
 #pragma unroll
-    for (int c = 0; c < CHUNKS; ++c) {
-        const int64_t e = e0 + 128 * c + 4 * lane;
-        const int nv = FULL ? 4 : nvalid4(ne, 128 * c + 4 * lane);
+    for (int r = 0; r < R; ++r) L.wv[r] = lane < nw ? ld_word(h.gathered + r * a.stride + w0 + lane) : 0u;
+#pragma unroll
+    for (int c = 0; c < CH; ++c) {
+        const int64_t e = e0 + 128 * (c0 + c) + 4 * lane;
+        const int nv = FULL ? 4 : nvalid4(ne, 128 * (c0 + c) + 4 * lane);
+        ldw4(static_cast<const TW*>(h.W) + e, nv, L.wt[c]);
+        if (do_loc) L.gt[c] = ld_stream_m(h.gnext + e, nv);
+    }
+}
+template <int NR, typename TW, bool FULL, int CH>
+__device__ __forceinline__ void apply_vec_tile(const ApplyQArgs& a, const K2Hot& h, const float* s_upd,
+                                               const double* s_upd64, int nr, int lane, int64_t e0, int64_t w0, int ne,
+                                               int nw, int c0, bool do_loc, int so0, int64_t sbnd, bool a_off,
+                                               int& isq, double& gsq2, uint64_t& bad_idx, K2Regs<NR, TW, CH>& L,
+                                               bool loaded) {
+    constexpr int R = NR > 0 ? NR : 1;
+    constexpr bool SINK = CH == 1;  // small layouts: aborted rounds store to the sink (no branch, see fused_vec_task)
+    TW* const W = static_cast<TW*>(h.W);
+    if (CH != 1 || !loaded) apply_vec_load<NR, TW, FULL, CH>(a, h, lane, e0, w0, ne, nw, c0, do_loc, L);
+    uint32_t(&wv)[R] = L.wv;
+    WV<TW>(&wt)[CH] = L.wt;
+    float4(&gt)[CH] = L.gt;
+    const int a_on = a_off ? 0 : 1;
+#pragma unroll
+    for (int c = 0; c < CH; ++c) {
+        const int64_t e = e0 + 128 * (c0 + c) + 4 * lane;
+        const int nv = FULL ? 4 : nvalid4(ne, 128 * (c0 + c) + 4 * lane);
         Counts cnt{0u, 0u, 0u, 0u, 0u};
 #pragma unroll
-        for (int r = 0; r < R; ++r) count_add(cnt, __shfl_sync(FULL, wv[r], 8 * c + (lane >> 2)));
+        for (int r = 0; r < R; ++r) count_add(cnt, __shfl_sync(FULL, wv[r], 8 * (c0 + c) + (lane >> 2)));
         const int jb = 4 * (lane & 3);  // first code position of this lane in the word
         WV<TW>& w4 = wt[c];
         float g4[4];
@@ -700,23 +744,24 @@ __device__ __forceinline__ void apply_vec_tile(const ApplyQArgs& a, const float*
         for (int q = 0; q < 4; ++q) {
             w4.v[q] = w_sub_tab(w4.v[q], s_upd, s_upd64, cq[q] + nr);
             if (do_loc) l4[q] = loc_of(w4.v[q], g4[q], a.eta_l, a.eta_l_d);
-            isq += cq[q] * cq[q];
+            isq += a_on * cq[q] * cq[q];
             if (a.fold) {  // N=1 correction round t+1: W_{t+2} = W_{t+1} - eta*g_{t+1} (mean = g itself)
                 w4.v[q] = w_sub_full(w4.v[q], g4[q], a.fold_scale, a.eta_g_d, 1.0, 1);
                 const double m = static_cast<double>(g4[q]);
-                gsq2 = __fma_rn(m, m, gsq2);  // (a two-chain tree measured 2 us slower)
+                if (!SINK || !a_off) gsq2 = __fma_rn(m, m, gsq2);  // (a two-chain tree measured 2 us slower)
             }
         }
         const uint32_t vm = nv >= 4 ? 0xffu : (1u << (2 * nv)) - 1u;  // padding codes are not checked
-        if (((cnt.rsv >> (2 * jb)) & vm) != 0u) {
+        if (!a_off && ((cnt.rsv >> (2 * jb)) & vm) != 0u) {
             const int q = __ffs((cnt.rsv >> (2 * jb)) & vm & 0x55u) / 2;
             const uint64_t idx = static_cast<uint64_t>(e + q);
             bad_idx = idx < bad_idx ? idx : bad_idx;
         }
         if (nv > 0) {
-            stw4(W + e, w4, nv);
-            if (do_loc) st_stream_m(a.loc + e, l4[0], l4[1], l4[2], l4[3], nv);
-            if (a.gs.chunk != 0) st_stream_m(stage_at(a.gs, e, so0, sbnd), g4[0], g4[1], g4[2], g4[3], nv);
+            stw4(SINK && a_off ? sink_of<TW>(h.sink, lane) : W + e, w4, nv);
+            if (do_loc)
+                st_stream_m(SINK && a_off ? sink_of<float>(h.sink, lane) : h.loc + e, l4[0], l4[1], l4[2], l4[3], nv);
+            if (a.gs.chunk != 0 && !a_off) st_stream_m(stage_at(a.gs, e, so0, sbnd), g4[0], g4[1], g4[2], g4[3], nv);
         }
     }
 }
@@ -727,11 +772,15 @@ __device__ __forceinline__ void apply_vec_tile(const ApplyQArgs& a, const float*
 // WIDE = 1: one 512-thread CTA per SM (the same 16 warps and register budget as 2 x 256), so
 // a grid of (SMs - R) CTAs leaves R whole SMs free — launched beside a correction all-reduce,
 // whose NCCL CTAs (104 KB smem, 52K registers each) cannot share an SM with this kernel.
+// CH = chunks of 128 elements per task: 4 (a whole tile) for large layouts, 1 for small ones
+// (4x the warps in flight; the first task's loads issued straight after the wait, as in
+// k_fused_ldg).
 #ifndef CDSGD_K2_MINB
 #define CDSGD_K2_MINB (NR == 1 && sizeof(TW) == 4 ? 3 : 2)
 #endif
-template <int NR, int WIDE = 0, typename TW = float>
+template <int NR, int WIDE = 0, typename TW = float, int CH = CHUNKS>
 __global__ void __launch_bounds__(WIDE ? 512 : 256, WIDE ? 1 : CDSGD_K2_MINB) k_apply_quant(ApplyQArgs a, KeyTab kt, DecodeTab tab) {
+    constexpr int SPL = CHUNKS / CH;  // tasks per tile
     __shared__ double s_mean[2 * MAX_RANKS + 1];
     __shared__ double s_upd64[2 * MAX_RANKS + 1];
     __shared__ float s_upd[2 * MAX_RANKS + 1];
@@ -742,73 +791,120 @@ __global__ void __launch_bounds__(WIDE ? 512 : 256, WIDE ? 1 : CDSGD_K2_MINB) k_
         s_upd[threadIdx.x] = tab.upd[threadIdx.x];
         s_upd64[threadIdx.x] = tab.upd64[threadIdx.x];
     }
+    const int64_t ntasks = kt.ntiles * SPL;
     int64_t tb, te;
-    warp_range(kt.ntiles, tb, te);
+    warp_range(ntasks, tb, te);
     const int lane = threadIdx.x & 31;
     double gsq = 0.0, gsq2 = 0.0;
     int isq = 0;  // sum of cnt^2 on the table path: gsq += isq * (alpha/N)^2
     uint64_t bad_idx = NO_ERR;
     const bool do_loc = a.loc != nullptr;
-    // small layouts (fewer than ~4 tiles per warp): claim single tiles for parallelism
+    // small layouts (fewer than ~4 tasks per warp): claim single tasks for parallelism
     const int64_t nwarps = (int64_t)gridDim.x * blockDim.x / 32;
-    const unsigned CLAIM = kt.ntiles < 4 * nwarps ? 1u : 2u;
-    const int64_t tail_from = kt.ntiles - nwarps;  // single-tile claims from here on
+    const unsigned CLAIM = ntasks < 4 * nwarps ? 1u : 2u;
+    const int64_t tail_from = ntasks - nwarps;  // single-task claims from here on
     // one wave of tasks (small layouts): each warp takes its own, no ticket and no end-of-launch
     // ticket reset (a fence + atomic per CTA on one counter)
-    const bool dyn = a.sched != nullptr && kt.ntiles > nwarps * static_cast<int64_t>(CLAIM);
+    bool dyn = a.sched != nullptr && ntasks > nwarps * static_cast<int64_t>(CLAIM);
     int64_t cend = 0;
     const int64_t first_dyn = nwarps * CLAIM;  // first claim static, then tickets (see k_fused_ldg)
     if (dyn) {
         tb = ((static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5) * CLAIM;
-        cend = tb + (int64_t)CLAIM < kt.ntiles ? tb + (int64_t)CLAIM : kt.ntiles;
-        te = tb < kt.ntiles ? kt.ntiles : tb;
+        cend = tb + (int64_t)CLAIM < ntasks ? tb + (int64_t)CLAIM : ntasks;
+        te = tb < ntasks ? ntasks : tb;
     }
     // constant inputs (tables, schedule, key seek) before griddepcontrol.wait (see k_fused_ldg)
     TileCursor kc;
     if (tb < te) {
-        if (kt.tiles != nullptr) kc.from_table(kt, tb);
-        else kc.seek_warp(kt, tb, lane);
+        if (kt.tiles != nullptr) kc.from_table(kt, tb / SPL);
+        else kc.seek_warp(kt, tb / SPL, lane);
     }
+    struct TaskDesc {
+        int64_t e0, w0;
+        int ne, nw, c0;
+        bool fast;
+    };
+    auto describe = [&](int64_t task) {
+        TaskDesc d;
+        const int64_t ti = task / SPL;
+        d.c0 = static_cast<int>(task % SPL) * CH;
+        if (kt.tiles != nullptr) kc.from_table(kt, ti);
+        else kc.advance_warp(kt, ti, lane);
+        const int64_t j = ti - kc.t0;
+        d.e0 = kc.e0 + j * TILE_ELEMS;
+        d.w0 = kc.w0 + j * TILE_WORDS;
+        const int64_t ne64 = kc.e1 - d.e0;
+        d.ne = ne64 < TILE_ELEMS ? static_cast<int>(ne64) : TILE_ELEMS;
+        const int64_t nw64 = kc.w1 - d.w0;
+        d.nw = nw64 < TILE_WORDS ? static_cast<int>(nw64) : TILE_WORDS;
+        d.fast = NR > 0 && a.exact && aligned_to(W + d.e0, 4 * sizeof(TW)) &&
+                 (!do_loc || (aligned_to(a.gnext + d.e0, 16) && aligned_to(a.loc + d.e0, 16)));
+        return d;
+    };
+    TaskDesc td{};
+    if (CH == 1 && tb < te) td = describe(tb);
+    K2Hot hot(a);
+    if constexpr (CH == 1) {
+        hot.pin_here();
+        int d = dyn ? 1 : 0;
+        asm volatile("" : "+r"(d));
+        dyn = d != 0;
+    }
+    if constexpr (CH == 1) __syncthreads();  // s_mean / s_upd, before the wait
     pdl_enter(a.gclear[0], a.gclear[1]);
-    const bool peer_failed = p2p_wait2(a.x, a.xs);
-    const bool skip = peer_failed || (a.err != nullptr && *reinterpret_cast<volatile uint64_t*>(a.err) < a.skip_below);
-    __syncthreads();
-    if (tb < te && !skip) {
-        for (int64_t ti = tb; ti < te; ++ti) {
-            if (dyn && ti >= cend) {
-                const unsigned cl = ti < tail_from ? CLAIM : 1u;
+    K2Regs<NR, TW, CH> L;
+    bool pre = false;
+    if constexpr (CH == 1) {  // first task's loads right after the wait (not behind a peer-flag wait)
+        pre = tb < te && td.fast && !hot.p2p_wait;
+        if (pre) {
+            if (td.ne == TILE_ELEMS)
+                apply_vec_load<NR, TW, true, CH>(a, hot, lane, td.e0, td.w0, td.ne, td.nw, td.c0, do_loc, L);
+            else
+                apply_vec_load<NR, TW, false, CH>(a, hot, lane, td.e0, td.w0, td.ne, td.nw, td.c0, do_loc, L);
+        }
+    }
+    const bool peer_failed = (CH != 1 || hot.p2p_wait) && p2p_wait2(a.x, a.xs);
+    bool skip;
+    if constexpr (CH == 1) {  // error word read after the loads went out (weak load, see RoundFlags)
+        uint64_t e0v = ~0ull;
+        if (a.err != nullptr) asm volatile("ld.global.u64 %0, [%1];" : "=l"(e0v) : "l"(a.err) : "memory");
+        skip = peer_failed || e0v < a.skip_below;
+    } else {
+        skip = peer_failed || (a.err != nullptr && *reinterpret_cast<volatile uint64_t*>(a.err) < a.skip_below);
+        __syncthreads();
+    }
+    if (tb < te && (CH == 1 || !skip)) {
+        for (int64_t task = tb; task < te; ++task) {
+            if (dyn && task >= cend) {
+                const unsigned cl = task < tail_from ? CLAIM : 1u;
                 unsigned t0 = 0;
                 if (lane == 0) t0 = atomicAdd(a.sched, cl);
                 const int64_t nb = first_dyn + static_cast<int64_t>(__shfl_sync(FULL, t0, 0));
-                if (nb >= kt.ntiles) break;
-                ti = nb;
-                cend = nb + (int64_t)cl < kt.ntiles ? nb + (int64_t)cl : kt.ntiles;
+                if (nb >= ntasks) break;
+                task = nb;
+                cend = nb + (int64_t)cl < ntasks ? nb + (int64_t)cl : ntasks;
             }
-            if (kt.tiles != nullptr) kc.from_table(kt, ti);
-            else kc.advance_warp(kt, ti, lane);
-            const int64_t j = ti - kc.t0;
-            const int64_t e0 = kc.e0 + j * TILE_ELEMS;
-            const int64_t w0 = kc.w0 + j * TILE_WORDS;
-            const int64_t ne64 = kc.e1 - e0;
-            const int ne = ne64 < TILE_ELEMS ? static_cast<int>(ne64) : TILE_ELEMS;
-            const int64_t nw64 = kc.w1 - w0;
-            const int nw = nw64 < TILE_WORDS ? static_cast<int>(nw64) : TILE_WORDS;
-            const bool fast = NR > 0 && a.exact && aligned_to(W + e0, 4 * sizeof(TW)) &&
-                              (!do_loc || (aligned_to(a.gnext + e0, 16) && aligned_to(a.loc + e0, 16)));
+            if (CH != 1 || task != tb) td = describe(task);
+            const int64_t e0 = td.e0, w0 = td.w0;
+            const int ne = td.ne, nw = td.nw, c0 = td.c0;
+            const bool fast = td.fast;
+            if (!fast && c0 != 0) continue;  // misaligned tiles: one task does the whole tile
             int so0 = 0;
             int64_t sbnd = 0;
             if (a.gs.chunk != 0) {
                 so0 = static_cast<int>(e0 / a.gs.chunk);
                 sbnd = (so0 + 1) * a.gs.chunk;
             }
+            const bool a_off = CH == 1 && skip;  // (large layouts: the loop only runs when !skip)
             if (fast) {
+                const bool loaded = pre && task == tb;
                 if (ne == TILE_ELEMS)
-                    apply_vec_tile<NR, TW, true>(a, s_upd, s_upd64, nr, lane, e0, w0, ne, nw, do_loc, so0, sbnd, isq,
-                                                 gsq2, bad_idx);
+                    apply_vec_tile<NR, TW, true, CH>(a, hot, s_upd, s_upd64, nr, lane, e0, w0, ne, nw, c0, do_loc, so0,
+                                                     sbnd, a_off, isq, gsq2, bad_idx, L, loaded);
                 else
-                    apply_vec_tile<NR, TW, false>(a, s_upd, s_upd64, nr, lane, e0, w0, ne, nw, do_loc, so0, sbnd, isq,
-                                                  gsq2, bad_idx);
-            } else {
+                    apply_vec_tile<NR, TW, false, CH>(a, hot, s_upd, s_upd64, nr, lane, e0, w0, ne, nw, c0, do_loc, so0,
+                                                      sbnd, a_off, isq, gsq2, bad_idx, L, loaded);
+            } else if (!a_off) {
                 // generic path: lane l owns element 32s + l; word (2s + l/16), code l%16
                 uint32_t wv[MAX_RANKS];
                 const bool wl = lane < nw;

@@ -53,13 +53,6 @@ struct FusedArgs {
     double* gclear[2];    // grad-norm ring slots to zero (see pdl_enter), nullable
 };
 
-// Write-only scratch for the stores of an aborted round on the branch-free small-layout path
-// (32 lanes x 32 bytes; concurrent garbage writes from every warp are harmless).
-__device__ __align__(32) double g_sink[32 * 4];
-template <typename T>
-__device__ __forceinline__ T* sink_of(double* sink, int lane) {
-    return reinterpret_cast<T*>(sink + 4 * lane);
-}
 
 // The pointers a task's loads and stores need, held in registers from BEFORE the
 // grid-dependency wait: read from the kernel parameters after it, they were constant-bank
