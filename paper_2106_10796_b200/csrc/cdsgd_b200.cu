@@ -11,6 +11,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <string>
 #include <vector>
 
 #include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: a no-op unless a profiler is attached
@@ -784,7 +785,18 @@ extern "C" int cdsgd_comm_init(const void* uid, int32_t nranks, int32_t rank, cd
         cfg.minCTAs = min_ctas;
         cfg.maxCTAs = min_ctas;  // the default cap is below 64 (ncclInvalidArgument otherwise)
     }
+    // CDSGD_NCCL_ALGO: an NCCL_ALGO value for this communicator only (e.g. "allreduce:nvls" for
+    // the fp32 correction all-reduce), set around its creation so the framework's own
+    // communicators (fp64 all-reduces, broadcasts) keep every algorithm (development A/B)
+    const char* algo = getenv("CDSGD_NCCL_ALGO");
+    const char* prev = getenv("NCCL_ALGO");
+    std::string prev_s = prev != nullptr ? prev : "";
+    if (algo != nullptr) setenv("NCCL_ALGO", algo, 1);
     ncclResult_t r = ncclCommInitRankConfig(&c->nccl, nranks, id, rank, &cfg);
+    if (algo != nullptr) {
+        if (prev != nullptr) setenv("NCCL_ALGO", prev_s.c_str(), 1);
+        else unsetenv("NCCL_ALGO");
+    }
     if (r != ncclSuccess) {
         delete c;
         return fail(CDSGD_ERR_NCCL, "ncclCommInitRankConfig: %s", ncclGetErrorString(r));
