@@ -565,12 +565,13 @@ int launch_apply_quant(const cdsgd_layout* L, void* W, int wdt, const uint32_t* 
         LAUNCH_CHECK();
         return CDSGD_OK;
     }
-    // small layouts (fewer than ~2 whole tiles per resident warp): one 128-element chunk per
-    // warp task, as the fused kernel (4x the warps in flight)
+    // one-wave layouts (a 128-element chunk task for every resident warp or fewer): chunk tasks,
+    // as the fused kernel (4x the warps in flight). Above that whole tiles: at 2^20 elements
+    // (4 chunk tasks per warp) chunk tasks measured 17 vs 11 us.
 #define AQ(R, TW)                                                                                       \
     case R:                                                                                             \
-        if (kt.ntiles < ch1_tiles_per_warp() * static_cast<int64_t>(resident_blocks(k_apply_quant<R, 0, TW>, THREADS)) * \
-                            WARPS_PER_BLOCK)                                                            \
+        if (kt.ntiles * CHUNKS <= static_cast<int64_t>(resident_blocks(k_apply_quant<R, 0, TW, 1>, THREADS)) * \
+                                      WARPS_PER_BLOCK)                                                  \
             launch_pdl(k_apply_quant<R, 0, TW, 1>,                                                      \
                        std::min(tile_grid(k_apply_quant<R, 0, TW, 1>, kt.ntiles * CHUNKS), small_grid_cap()), THREADS, \
                        0, st, a, kt, tab);                                                              \

@@ -138,12 +138,22 @@ def test_engine_numeric_error_rolls_back_residual(pkg):
     good = wk.residual.clone()
     g = torch.from_numpy(O.synthetic_grad(3, 2, 0, layout.total)).cuda()
     g[640 + 42] = float("nan")
-    wk.step(g)  # round 2: compressed, poisoned
+    wk.step(g)  # round 2: compressed, poisoned (its apply of round 1 is valid)
+    w_before, loc_before = wk.weights.clone(), wk.compute_weights().clone()
     wk.step(torch.from_numpy(O.synthetic_grad(3, 3, 0, layout.total)).cuda())  # round 3: correction
     with pytest.raises(CodecNumericError) as ei:
         wk.check()
     assert (ei.value.key, ei.value.index, ei.value.round) == (1, 42, 2)
     assert torch.equal(wk.residual, good), "residual must be the one valid before the failing round"
+    # the apply of the failed round is skipped (sticky abort; small-layout kernels send those
+    # stores to a sink instead of branching): W and the compute weights stay as they were
+    # (bitwise: the compute weights of the poisoned round hold its NaN, loc = W - eta_l * g)
+    def bits(x):
+        return x.view(torch.int64 if x.dtype == torch.float64 else torch.int32)
+
+    assert torch.equal(bits(wk.weights), bits(w_before)), "W must not move after the failing round"
+    assert torch.equal(bits(wk.compute_weights()), bits(loc_before)), \
+        "compute weights must not move after the failing round"
     with pytest.raises(Exception):
         wk.step(g)
 
