@@ -1,6 +1,10 @@
 #!/bin/bash
+# ncu --set full of the small-layout (ResNet-20) kernels, graph replays, caches not flushed
+# (the round's inputs are L2-resident in steady state), then the N=1 sweep
 mkdir -p gpurun_out
-C="python bench.py --workload resnet20 --steps 8 --warmup 4 --no-cpu-baseline --no-e2e --no-secondary --no-self-check"
-timeout 300 $C > gpurun_out/${TAG}_plain.log 2>&1 && \
-timeout 300 ncu --metrics gpu__time_duration.sum,launch__grid_size,sm__cycles_active.avg,sm__cycles_elapsed.avg --clock-control none -k regex:k_ -c 40 --csv --log-file gpurun_out/${TAG}_launches.csv $C > gpurun_out/${TAG}_ncu.log 2>&1
-echo "ncu rc=$?"
+timeout 900 ncu --set full --import-source on --clock-control none --cache-control none -k "regex:k_fused|k_apply_quant" -s 200 -c 6 \
+  -o gpurun_out/${TAG}_r20 python scripts/small_probe.py --periods 10 --reps 20 > gpurun_out/${TAG}_ncu.log 2>&1; echo "ncu rc=$?"
+ncu -i gpurun_out/${TAG}_r20.ncu-rep --page raw --csv > gpurun_out/${TAG}_r20_raw.csv 2>/dev/null
+ncu -i gpurun_out/${TAG}_r20.ncu-rep --page details > gpurun_out/${TAG}_r20_details.txt 2>/dev/null
+rm -f gpurun_out/${TAG}_r20.ncu-rep
+SKIP_MGPU=1 bash scripts/sweep_configs.sh
