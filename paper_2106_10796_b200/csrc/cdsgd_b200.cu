@@ -789,14 +789,30 @@ extern "C" int cdsgd_comm_init(const void* uid, int32_t nranks, int32_t rank, cd
     // CDSGD_NCCL_ALGO: an NCCL_ALGO value for this communicator only (e.g. "allreduce:nvls" for
     // the fp32 correction all-reduce), set around its creation so the framework's own
     // communicators (fp64 all-reduces, broadcasts) keep every algorithm (development A/B)
-    const char* algo = getenv("CDSGD_NCCL_ALGO");
-    const char* prev = getenv("NCCL_ALGO");
-    std::string prev_s = prev != nullptr ? prev : "";
-    if (algo != nullptr) setenv("NCCL_ALGO", algo, 1);
-    ncclResult_t r = ncclCommInitRankConfig(&c->nccl, nranks, id, rank, &cfg);
-    if (algo != nullptr) {
-        if (prev != nullptr) setenv("NCCL_ALGO", prev_s.c_str(), 1);
-        else unsetenv("NCCL_ALGO");
+    // (CDSGD_NCCL_PROTO likewise for NCCL_PROTO)
+    struct ScopedEnv {
+        const char* name;
+        bool set = false, had = false;
+        std::string prev;
+        ScopedEnv(const char* n, const char* v) : name(n) {
+            if (v == nullptr) return;
+            const char* p = getenv(n);
+            had = p != nullptr;
+            if (had) prev = p;
+            setenv(n, v, 1);
+            set = true;
+        }
+        ~ScopedEnv() {
+            if (!set) return;
+            if (had) setenv(name, prev.c_str(), 1);
+            else unsetenv(name);
+        }
+    };
+    ncclResult_t r;
+    {
+        const ScopedEnv algo("NCCL_ALGO", getenv("CDSGD_NCCL_ALGO"));
+        const ScopedEnv proto("NCCL_PROTO", getenv("CDSGD_NCCL_PROTO"));
+        r = ncclCommInitRankConfig(&c->nccl, nranks, id, rank, &cfg);
     }
     if (r != ncclSuccess) {
         delete c;
