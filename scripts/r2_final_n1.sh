@@ -11,6 +11,6 @@ for f in ("gpurun_out/${TAG}_ref.log","gpurun_out/${TAG}_bench.log"):
     l=[x for x in open(f) if x.startswith("{")]
     d=json.loads(l[-1]); print(f, d.get("impl","ours"), "value", round(d["value"],2), "e2e", round(d["e2e"]["value"],2), "clocks", d.get("clocks"))
     if "secondary" in d:
-        r=d["secondary"]["resnet20"]; print("  r20 host", round(r["value"],1), "graph", round(r["cuda_graph"]["value"],1), "graph1", round(r["cuda_graph"]["one_period_per_graph"]["value"],1), "cold", round(r["cold_l2"]["value"],1))
+        r=d["secondary"]["resnet20"]; print("  r20 host", round(r["value"],1), "graph", round(r["cuda_graph"]["value"],1), "graph1", round(r["cuda_graph"]["one_period_per_graph"]["value"],1), "cold", round(r["cold_l2"]["value"],1), "cold graph", r["cold_l2"].get("cuda_graph"))
         print("  roofline", d["roofline"], "selfcheck", d.get("self_check",{}).get("ok"))
 PY
