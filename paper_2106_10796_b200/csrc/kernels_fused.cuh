@@ -79,30 +79,6 @@ struct HotPtrs {
     }
 };
 
-// Touch, before the grid-dependency wait, every kernel-parameter field the small-layout path
-// reads after it: the first read of a parameter line is a constant-cache miss, and after the
-// wait every warp of the grid would take those misses on its way to its loads (~900 cycles
-// measured between the wait's release and the first data load on ResNet-20-sized layouts).
-// The values are folded into one register that an opaque asm consumes here; the later reads
-// hit the constant cache.
-__device__ __forceinline__ void warm_params(const FusedArgs& a, const DecodeTab& tab) {
-    uint64_t w = static_cast<uint64_t>(a.stride) ^ a.tag ^ a.skip_below ^ static_cast<uint64_t>(a.exact) ^
-                 static_cast<uint64_t>(a.nranks) ^ __float_as_uint(a.eta_l) ^ __double_as_longlong(a.eta_l_d) ^
-                 __double_as_longlong(a.alpha) ^ reinterpret_cast<uint64_t>(a.gnorm) ^
-                 reinterpret_cast<uint64_t>(a.words) ^ reinterpret_cast<uint64_t>(a.sched) ^
-                 reinterpret_cast<uint64_t>(a.gclear[0]) ^ reinterpret_cast<uint64_t>(a.gclear[1]) ^
-                 __double_as_longlong(tab.sq_scale);
-    const P2PArgs* xs[2] = {&a.xq, &a.xa};
-#pragma unroll
-    for (int i = 0; i < 2; ++i) {
-        const P2PArgs& x = *xs[i];
-        w ^= static_cast<uint64_t>(x.nranks) ^ reinterpret_cast<uint64_t>(x.wait_flags) ^ x.wait_value ^
-             x.publish_value ^ reinterpret_cast<uint64_t>(x.counter) ^ reinterpret_cast<uint64_t>(x.dst[0]) ^
-             reinterpret_cast<uint64_t>(x.publish[0]) ^ static_cast<uint64_t>(x.sc_fence);
-    }
-    asm volatile("" ::"l"(w));
-}
-
 // Development probe (-DCDSGD_PROBE_TIMING builds only, loaded through CDSGD_LIB): per-warp
 // clock64 stamps of the launch's phases, read back by cdsgd_diag_probe (scripts/small_probe.py).
 #ifdef CDSGD_PROBE_TIMING
@@ -436,10 +412,7 @@ __global__ void __launch_bounds__(256, sizeof(TW) == 8 ? CDSGD_F64_MINB : 2) k_f
     TaskDesc td{};
     if (CH == 1 && tb < te) td = describe(tb);  // (large layouts: in the loop, fewer live registers)
     HotPtrs hot(a);
-    if constexpr (CH == 1) {
-        hot.pin_here();
-        warm_params(a, tab);
-    }
+    if constexpr (CH == 1) hot.pin_here();
     if (APPLY == APPLY_Q) __syncthreads();  // s_upd, before the wait (off the critical path)
     CDSGD_PROBE(2);
     pdl_enter(a.gclear[0], a.gclear[1]);  // from here on: memory the preceding kernels write
