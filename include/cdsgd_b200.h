@@ -238,7 +238,7 @@ int cdsgd_engine_check(cdsgd_engine* eng, void* stream, int64_t* round, int64_t*
 int cdsgd_engine_round_compressed(const cdsgd_engine* eng, int64_t t);
 /* Fused NVLink exchange (replaces the NCCL all-gather of codes on compressed rounds).
  * Every rank allocates one symmetric buffer of cdsgd_p2p_bytes(nranks, n, words) bytes
- * (zero-filled; e.g. torch symmetric memory), maps all peers' buffers, and passes
+ * (zero-filled; cdsgd_p2p_buffer_alloc/_open below, or torch symmetric memory), maps all peers' buffers, and passes
  * the nranks base addresses (index = rank, 256-byte aligned) before round 0. K1 then
  * stores each packed word directly into every rank's slot and publishes a release
  * flag; K2 acquires all ranks' flags (spin on local memory, ~10 s timeout ->
@@ -257,6 +257,15 @@ int64_t cdsgd_p2p_bytes(int32_t nranks, int64_t n, int64_t words);
  * peers store their W' shards of correction rounds into it). */
 int64_t cdsgd_p2p_weights_offset(int32_t nranks, int64_t n, int64_t words);
 int cdsgd_engine_attach_p2p(cdsgd_engine* eng, void* const* peer_bases, int32_t nranks, int32_t exact_correction);
+/* A symmetric buffer without torch: cudaMalloc'd and zero-filled on the current device,
+ * with its CUDA IPC handle (CDSGD_P2P_HANDLE_BYTES bytes) for the other ranks of the box;
+ * _open maps a peer's buffer (peer access enabled on first use), _close unmaps it, _free
+ * releases the local one (after every rank has stopped using it). */
+#define CDSGD_P2P_HANDLE_BYTES 64
+int cdsgd_p2p_buffer_alloc(int64_t bytes, void** ptr, void* handle);
+int cdsgd_p2p_buffer_open(const void* handle, void** ptr);
+int cdsgd_p2p_buffer_close(void* peer_ptr);
+int cdsgd_p2p_buffer_free(void* ptr);
 /* Make `stream` wait for every exchange the engine has issued so far. */
 int cdsgd_engine_join(cdsgd_engine* eng, void* stream);
 /* Per-kernel timing with CUDA events recorded on the launching streams around

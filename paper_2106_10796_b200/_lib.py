@@ -89,12 +89,17 @@ _SIGS = {
     "cdsgd_p2p_bytes": (i64, [i32, i64, i64]),
     "cdsgd_p2p_weights_offset": (i64, [i32, i64, i64]),
     "cdsgd_engine_attach_p2p": (C.c_int, [vp, C.POINTER(vp), i32, i32]),
+    "cdsgd_p2p_buffer_alloc": (C.c_int, [i64, C.POINTER(vp), vp]),
+    "cdsgd_p2p_buffer_open": (C.c_int, [vp, C.POINTER(vp)]),
+    "cdsgd_p2p_buffer_close": (C.c_int, [vp]),
+    "cdsgd_p2p_buffer_free": (C.c_int, [vp]),
     "cdsgd_engine_profile_begin": (C.c_int, [vp]),
     "cdsgd_engine_profile_end": (C.c_int, [vp, C.POINTER(f64)]),
     "cdsgd_engine_ce_fraction": (C.c_double, [vp]),
 }
 
 EXPORTED_SYMBOLS = tuple(_SIGS)
+P2P_HANDLE_BYTES = 64  # CDSGD_P2P_HANDLE_BYTES (a cudaIpcMemHandle_t)
 
 _lib = None
 

@@ -1502,6 +1502,43 @@ extern "C" int64_t cdsgd_p2p_weights_offset(int32_t nranks, int64_t n, int64_t w
     return off[4];
 }
 
+// Native symmetric buffer: cudaMalloc'd, zero-filled, exported as a CUDA IPC handle that
+// the other ranks of the box map with cudaIpcOpenMemHandle (peer access enabled lazily).
+static_assert(sizeof(cudaIpcMemHandle_t) == CDSGD_P2P_HANDLE_BYTES, "IPC handle size");
+extern "C" int cdsgd_p2p_buffer_alloc(int64_t bytes, void** ptr, void* handle) {
+    if (ptr == nullptr || handle == nullptr || bytes <= 0) return fail(CDSGD_ERR_ARG, "bad p2p buffer arguments");
+    void* p = nullptr;
+    CUDA_TRY(cudaMalloc(&p, static_cast<size_t>(bytes)));
+    cudaError_t e = cudaMemset(p, 0, static_cast<size_t>(bytes));
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    cudaIpcMemHandle_t h{};
+    if (e == cudaSuccess) e = cudaIpcGetMemHandle(&h, p);
+    if (e != cudaSuccess) {
+        cudaFree(p);
+        return fail(CDSGD_ERR_CUDA, "p2p buffer: %s", cudaGetErrorString(e));
+    }
+    std::memcpy(handle, &h, sizeof(h));
+    *ptr = p;
+    return CDSGD_OK;
+}
+extern "C" int cdsgd_p2p_buffer_open(const void* handle, void** ptr) {
+    if (ptr == nullptr || handle == nullptr) return fail(CDSGD_ERR_ARG, "NULL argument");
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle, sizeof(h));
+    CUDA_TRY(cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess));
+    return CDSGD_OK;
+}
+extern "C" int cdsgd_p2p_buffer_close(void* peer_ptr) {
+    if (peer_ptr == nullptr) return CDSGD_OK;
+    CUDA_TRY(cudaIpcCloseMemHandle(peer_ptr));
+    return CDSGD_OK;
+}
+extern "C" int cdsgd_p2p_buffer_free(void* ptr) {
+    if (ptr == nullptr) return CDSGD_OK;
+    CUDA_TRY(cudaFree(ptr));
+    return CDSGD_OK;
+}
+
 extern "C" int cdsgd_engine_attach_p2p(cdsgd_engine* E, void* const* peer_bases, int32_t nranks,
                                        int32_t exact_correction) {
     if (E == nullptr || peer_bases == nullptr) return fail(CDSGD_ERR_ARG, "NULL argument");

@@ -25,6 +25,7 @@ key-local index and round; the residual is rolled back to the state before it.
 from __future__ import annotations
 
 import ctypes as C
+import os
 
 import numpy as np
 import torch
@@ -35,6 +36,14 @@ from .engine import ConfigError, HyperParams, SchedulingError
 from .layout import Layout
 
 _RAW_STREAM = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+
+
+class _CudaBytes:
+    """A raw device allocation seen as a uint8 CUDA array (torch.as_tensor aliases it)."""
+
+    def __init__(self, ptr: int, nbytes: int):
+        self.__cuda_array_interface__ = {"shape": (int(nbytes),), "typestr": "|u1", "data": (int(ptr), False),
+                                         "version": 3, "strides": None, "stream": None}
 
 
 def _raw_stream(index: int) -> int:
@@ -145,23 +154,32 @@ class CDSGDWorker:
         self._lib = _lib.lib()
 
     def _attach_p2p(self, group, exact: bool = False) -> None:
-        """Fused NVLink exchange: one symmetric buffer per rank (torch symmetric memory maps
-        every peer's buffer into this process); K1 stores codes straight into all ranks'
-        slots and K2 synchronises on release/acquire flags (cdsgd_engine_attach_p2p).
-        exact=True also replaces the correction all-reduce by the sharded fp64 NVLink reduce."""
+        """Fused NVLink exchange: one symmetric buffer per rank, every peer's buffer mapped into
+        this process; K1 stores codes straight into all ranks' slots and K2 synchronises on
+        release/acquire flags (cdsgd_engine_attach_p2p). exact=True also replaces the
+        correction all-reduce by the sharded fp64 NVLink reduce.
+
+        The buffers are the library's own (cudaMalloc + CUDA IPC handles exchanged over the
+        process group, cdsgd_p2p_buffer_*); CDSGD_P2P_MEMORY=torch uses torch's symmetric
+        memory instead (a private torch API)."""
         import torch.distributed as dist
-        import torch.distributed._symmetric_memory as symm_mem
 
         lib = _lib.lib()
         n, nw = self.layout.total, self.layout.n_words
         nbytes = int(lib.cdsgd_p2p_bytes(self.world, n, nw))
         w_off = int(lib.cdsgd_p2p_weights_offset(self.world, n, nw))
         grp = group if group is not None else dist.group.WORLD
-        self._symm = symm_mem.empty(nbytes, dtype=torch.uint8, device=self.device)
-        self._symm.zero_()
-        torch.cuda.synchronize(self.device)
-        self._symm_handle = symm_mem.rendezvous(self._symm, grp)
-        ptrs = [int(p) for p in self._symm_handle.buffer_ptrs]
+        self._p2p_group = grp
+        if os.environ.get("CDSGD_P2P_MEMORY", "native") == "torch":
+            import torch.distributed._symmetric_memory as symm_mem
+
+            self._symm = symm_mem.empty(nbytes, dtype=torch.uint8, device=self.device)
+            self._symm.zero_()
+            torch.cuda.synchronize(self.device)
+            self._symm_handle = symm_mem.rendezvous(self._symm, grp)
+            ptrs = [int(p) for p in self._symm_handle.buffer_ptrs]
+        else:
+            ptrs = self._native_symmetric(nbytes, grp)
         if len(ptrs) != self.world:
             raise ConfigError("symmetric memory group does not match hp.workers")
         arr = (C.c_void_p * self.world)(*ptrs)
@@ -174,6 +192,52 @@ class CDSGDWorker:
         self.gathered = [self._symm[i * slot:i * slot + self.world * nw * 4].view(torch.uint32) for i in range(2)]
         torch.cuda.synchronize(self.device)
         dist.barrier(group=grp)  # every rank's flags are zero before any rank's first K1
+
+    def _native_symmetric(self, nbytes: int, grp) -> list:
+        """Allocate this rank's buffer, all-gather the IPC handles, map the peers' buffers.
+        Returns the nranks base addresses (index = rank in the group)."""
+        import torch.distributed as dist
+
+        lib = _lib.lib()
+        with torch.cuda.device(self.device):
+            base = C.c_void_p()
+            handle = (C.c_uint8 * _lib.P2P_HANDLE_BYTES)()
+            _lib.check(lib.cdsgd_p2p_buffer_alloc(nbytes, C.byref(base), handle), "cdsgd_p2p_buffer_alloc")
+            self._p2p_base = base.value
+            handles = [None] * dist.get_world_size(grp)
+            dist.all_gather_object(handles, bytes(handle), group=grp)
+            me = dist.get_rank(grp)
+            ptrs = []
+            self._p2p_peers = []
+            for r, h in enumerate(handles):
+                if r == me:
+                    ptrs.append(base.value)
+                    continue
+                hb = (C.c_uint8 * _lib.P2P_HANDLE_BYTES).from_buffer_copy(h)
+                p = C.c_void_p()
+                _lib.check(lib.cdsgd_p2p_buffer_open(hb, C.byref(p)), "cdsgd_p2p_buffer_open")
+                self._p2p_peers.append(p.value)
+                ptrs.append(p.value)
+        self._symm = torch.as_tensor(_CudaBytes(base.value, nbytes), device=self.device)
+        return ptrs
+
+    def _release_symmetric(self) -> None:
+        """Unmap the peers' buffers and free this rank's (after every rank stopped using it)."""
+        base = getattr(self, "_p2p_base", None)
+        if base is None:
+            return
+        import torch.distributed as dist
+
+        torch.cuda.synchronize(self.device)
+        if dist.is_available() and dist.is_initialized():
+            dist.barrier(group=self._p2p_group)  # no rank's kernels still write into our buffer
+        lib = _lib.lib()
+        for p in self._p2p_peers:
+            lib.cdsgd_p2p_buffer_close(C.c_void_p(p))
+        self._p2p_peers = []
+        self._symm = self.W = self.gathered = None
+        lib.cdsgd_p2p_buffer_free(C.c_void_p(base))
+        self._p2p_base = None
 
     # ------------------------------------------------------------------ state
     def state(self) -> _lib.EngineState:
@@ -309,12 +373,19 @@ class CDSGDWorker:
         return {nm: {"ms": out[2 * i], "n": int(out[2 * i + 1])} for i, nm in enumerate(names)}
 
     def close(self) -> None:
+        """Destroy the engine; with the native symmetric buffer (P2P exchange) this is
+        collective: every rank calls it (the buffer is freed after a barrier)."""
         if getattr(self, "_eng", None):
             _lib.lib().cdsgd_engine_destroy(self._eng)
             self._eng = None
+        self._release_symmetric()
 
     def __del__(self):
         try:
-            self.close()
+            if getattr(self, "_eng", None):
+                _lib.lib().cdsgd_engine_destroy(self._eng)
+                self._eng = None
+            # a native symmetric buffer is only released by an explicit (collective) close();
+            # at interpreter exit the process's device memory goes with it
         except Exception:
             pass
