@@ -504,7 +504,6 @@ void build_tab(DecodeTab& tab, double alpha, double eta_g, int nr) {
 }
 inline bool pow2(int n) { return n > 0 && (n & (n - 1)) == 0; }
 
-int ch1_tiles_per_warp();
 int small_grid_cap();
 int launch_apply_quant(const cdsgd_layout* L, void* W, int wdt, const uint32_t* gathered, int nr, int64_t stride,
                        double alpha, double eta_g, const float* gnext, float* loc, double eta_l, uint64_t* err,
