@@ -649,9 +649,18 @@ int small_grid_cap() {
     }();
     return v;
 }
-template <int NR, int AP, typename TW, typename TR>
-int launch_fused_cfg(const FusedArgs& a, const KeyTab& kt, const DecodeTab& tab, cudaStream_t st) {
-    constexpr int CHL = sizeof(TW) == 8 ? CDSGD_F64_CH : CHUNKS;  // chunks per task on large layouts
+// Chunks per task of the fused kernel for several ranks' codes with fp64 weights: whole tiles
+// spill at 128 registers (F<4>: 120 B), half tiles do not — F 190 vs 194 us at N=4, 182 vs
+// 186 at N=2 (CDSGD_MR_CH=4 restores whole tiles). (K2 with half tiles measured no better.)
+bool mr_half_tiles() {
+    static const bool v = [] {
+        const char* e = getenv("CDSGD_MR_CH");
+        return e == nullptr || atoi(e) != 4;
+    }();
+    return v;
+}
+template <int NR, int AP, typename TW, typename TR, int CHL>
+int launch_fused_ch(const FusedArgs& a, const KeyTab& kt, const DecodeTab& tab, cudaStream_t st) {
     // fewer than 2 whole-tile tasks per resident warp: split tiles into chunk tasks
     const int64_t warps =
         static_cast<int64_t>(resident_blocks(k_fused_ldg<NR, AP, CHL, TW, TR>, THREADS)) * WARPS_PER_BLOCK;
@@ -663,6 +672,13 @@ int launch_fused_cfg(const FusedArgs& a, const KeyTab& kt, const DecodeTab& tab,
         launch_pdl(k_fused_ldg<NR, AP, CHL, TW, TR>,
                    tile_grid(k_fused_ldg<NR, AP, CHL, TW, TR>, kt.ntiles * (CHUNKS / CHL)), THREADS, 0, st, a, kt, tab);
     return CDSGD_OK;
+}
+template <int NR, int AP, typename TW, typename TR>
+int launch_fused_cfg(const FusedArgs& a, const KeyTab& kt, const DecodeTab& tab, cudaStream_t st) {
+    constexpr int CHL = sizeof(TW) == 8 ? CDSGD_F64_CH : CHUNKS;  // chunks per task on large layouts
+    if constexpr (sizeof(TW) == 8 && NR >= 2 && AP == APPLY_Q)
+        if (mr_half_tiles()) return launch_fused_ch<NR, AP, TW, TR, 2>(a, kt, tab, st);
+    return launch_fused_ch<NR, AP, TW, TR, CHL>(a, kt, tab, st);
 }
 template <typename TW, typename TR>
 int launch_fused_t(int nr, int apply, const FusedArgs& a, const KeyTab& kt, const DecodeTab& tab, cudaStream_t st) {
