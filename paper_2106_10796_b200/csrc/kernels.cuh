@@ -585,6 +585,12 @@ __device__ __forceinline__ float loc_of(double w, float g, float, double eta_l) 
 struct Counts {
     uint32_t pe, po, me, mo, rsv;
 };
+__device__ __forceinline__ void count_add(Counts& c, uint32_t w);
+// The counters of lane `src` (a word's counts summed over ranks, see fused_vec_task)
+__device__ __forceinline__ Counts shfl_counts(const Counts& w, int src) {
+    return Counts{__shfl_sync(FULL, w.pe, src), __shfl_sync(FULL, w.po, src), __shfl_sync(FULL, w.me, src),
+                  __shfl_sync(FULL, w.mo, src), __shfl_sync(FULL, w.rsv, src)};
+}
 __device__ __forceinline__ void count_add(Counts& c, uint32_t w) {
     c.pe += w & 0x11111111u;
     c.me += (w >> 1) & 0x11111111u;
@@ -698,7 +704,7 @@ struct K2Hot {
 // K2 vector path for one task: CH chunks of 128 elements (from chunk c0) of a tile (exact-alpha
 // table, compile-time rank count). Tiles of ne < TILE_ELEMS elements (a key's last) use masked
 // accesses; padding codes are ignored.
-template <int NR, typename TW, bool FULL, int CH>  // FULL: whole tile, unmasked accesses (see fused_vec_task)
+template <int NR, typename TW, bool WHOLE, int CH>  // WHOLE: whole tile, unmasked accesses (see fused_vec_task)
 __device__ __forceinline__ void apply_vec_load(const ApplyQArgs& a, const K2Hot& h, int lane, int64_t e0, int64_t w0,
                                                int ne, int nw, int c0, bool do_loc, K2Regs<NR, TW, CH>& L) {
     constexpr int R = NR > 0 ? NR : 1;
@@ -707,12 +713,12 @@ __device__ __forceinline__ void apply_vec_load(const ApplyQArgs& a, const K2Hot&
 #pragma unroll
     for (int c = 0; c < CH; ++c) {
         const int64_t e = e0 + 128 * (c0 + c) + 4 * lane;
-        const int nv = FULL ? 4 : nvalid4(ne, 128 * (c0 + c) + 4 * lane);
+        const int nv = WHOLE ? 4 : nvalid4(ne, 128 * (c0 + c) + 4 * lane);
         ldw4(static_cast<const TW*>(h.W) + e, nv, L.wt[c]);
         if (do_loc) L.gt[c] = ld_stream_m(h.gnext + e, nv);
     }
 }
-template <int NR, typename TW, bool FULL, int CH>
+template <int NR, typename TW, bool WHOLE, int CH>
 __device__ __forceinline__ void apply_vec_tile(const ApplyQArgs& a, const K2Hot& h, const float* s_upd,
                                                const double* s_upd64, int nr, int lane, int64_t e0, int64_t w0, int ne,
                                                int nw, int c0, bool do_loc, int so0, int64_t sbnd, bool a_off,
@@ -721,18 +727,27 @@ __device__ __forceinline__ void apply_vec_tile(const ApplyQArgs& a, const K2Hot&
     constexpr int R = NR > 0 ? NR : 1;
     constexpr bool SINK = CH == 1;  // small layouts: aborted rounds store to the sink (no branch, see fused_vec_task)
     TW* const W = static_cast<TW*>(h.W);
-    if (CH != 1 || !loaded) apply_vec_load<NR, TW, FULL, CH>(a, h, lane, e0, w0, ne, nw, c0, do_loc, L);
+    if (CH != 1 || !loaded) apply_vec_load<NR, TW, WHOLE, CH>(a, h, lane, e0, w0, ne, nw, c0, do_loc, L);
     uint32_t(&wv)[R] = L.wv;
     WV<TW>(&wt)[CH] = L.wt;
     float4(&gt)[CH] = L.gt;
     const int a_on = a_off ? 0 : 1;
+    Counts wc{0u, 0u, 0u, 0u, 0u};  // this lane's word, counts summed over the ranks (NR >= 2)
+    if constexpr (NR >= 2) {
+#pragma unroll
+        for (int r = 0; r < R; ++r) count_add(wc, wv[r]);
+    }
 #pragma unroll
     for (int c = 0; c < CH; ++c) {
         const int64_t e = e0 + 128 * (c0 + c) + 4 * lane;
-        const int nv = FULL ? 4 : nvalid4(ne, 128 * (c0 + c) + 4 * lane);
+        const int nv = WHOLE ? 4 : nvalid4(ne, 128 * (c0 + c) + 4 * lane);
         Counts cnt{0u, 0u, 0u, 0u, 0u};
+        if constexpr (NR >= 2) {
+            cnt = shfl_counts(wc, 8 * (c0 + c) + (lane >> 2));
+        } else {
 #pragma unroll
-        for (int r = 0; r < R; ++r) count_add(cnt, __shfl_sync(FULL, wv[r], 8 * (c0 + c) + (lane >> 2)));
+            for (int r = 0; r < R; ++r) count_add(cnt, __shfl_sync(FULL, wv[r], 8 * (c0 + c) + (lane >> 2)));
+        }
         const int jb = 4 * (lane & 3);  // first code position of this lane in the word
         WV<TW>& w4 = wt[c];
         float g4[4];

@@ -147,7 +147,7 @@ struct RoundFlags {
 // element e0 / word w0, all loads issued before any use. A key's last tile (ne < TILE_ELEMS
 // elements) uses masked accesses; padding quantizes to code 00 (the
 // reference's zero padding of the last word, codec.py:131-143) and is never stored.
-// FULL: a whole tile (ne == TILE_ELEMS), every access unmasked — the compiler drops the
+// WHOLE: a whole tile (ne == TILE_ELEMS), every access unmasked — the compiler drops the
 // masked-access branches and their registers (CDSGD_FULL_SPEC=0 disables the split).
 #ifndef CDSGD_FULL_SPEC
 #define CDSGD_FULL_SPEC 1
@@ -161,7 +161,7 @@ struct TaskRegs {
     uint32_t cw[APPLY == APPLY_Q ? NR : 1];
 };
 // Issue every load of a task (error word first on small layouts, see RoundFlags::issue).
-template <int NR, int APPLY, int CH, typename TW, bool FULL, typename TR>
+template <int NR, int APPLY, int CH, typename TW, bool WHOLE, typename TR>
 __device__ __forceinline__ void fused_vec_load(const FusedArgs& a, const HotPtrs& h, int lane, int64_t e0, int64_t w0,
                                                int ne, int nw, int c0, RoundFlags& fl,
                                                TaskRegs<NR, APPLY, CH, TW, TR>& L) {
@@ -175,7 +175,7 @@ __device__ __forceinline__ void fused_vec_load(const FusedArgs& a, const HotPtrs
 #pragma unroll
     for (int c = 0; c < CH; ++c) {
         const int64_t e = e0 + 128 * (c0 + c) + 4 * lane;
-        const int nv = FULL ? 4 : nvalid4(ne, 128 * (c0 + c) + 4 * lane);
+        const int nv = WHOLE ? 4 : nvalid4(ne, 128 * (c0 + c) + 4 * lane);
         L.gv[c] = ld_stream_m(h.g + e, nv);
         ldw4(static_cast<const TR*>(h.r_in) + e, nv, L.rv[c]);
         ldw4(static_cast<const TW*>(h.W) + e, nv, L.wv[c]);
@@ -183,7 +183,7 @@ __device__ __forceinline__ void fused_vec_load(const FusedArgs& a, const HotPtrs
     }
 }
 
-template <int NR, int APPLY, int CH, typename TW, bool FULL, typename TR>
+template <int NR, int APPLY, int CH, typename TW, bool WHOLE, typename TR>
 __device__ __forceinline__ uint32_t fused_vec_task(const FusedArgs& a, const HotPtrs& h, const float* s_upd, const double* s_upd64,
                                                    int lane, int64_t e0, int64_t w0, int ne, int nw, int c0,
                                                    RoundFlags& fl, uint32_t ahi, uint32_t alo,
@@ -192,7 +192,7 @@ __device__ __forceinline__ uint32_t fused_vec_task(const FusedArgs& a, const Hot
     uint32_t myword = 0;
     TW* const W = static_cast<TW*>(h.W);
     TR* const r_out = static_cast<TR*>(h.r_out);
-    if (CH != 1 || !loaded) fused_vec_load<NR, APPLY, CH, TW, FULL, TR>(a, h, lane, e0, w0, ne, nw, c0, fl, L);
+    if (CH != 1 || !loaded) fused_vec_load<NR, APPLY, CH, TW, WHOLE, TR>(a, h, lane, e0, w0, ne, nw, c0, fl, L);
     float4(&gv)[CH] = L.gv;
     float4(&sv)[CH] = L.sv;
     WV<TW>(&wv)[CH] = L.wv;
@@ -218,12 +218,19 @@ __device__ __forceinline__ uint32_t fused_vec_task(const FusedArgs& a, const Hot
     // behind the error word's round trip (two dependent trips per task instead of one).
     constexpr bool SINK = CH == 1;
     const int a_on = a_off ? 0 : 1;
+    // several ranks: each lane sums the counts of ITS word over the ranks once (the words of a
+    // chunk are read by 4 lanes each), then a chunk shuffles 5 counters instead of N words
+    Counts wc{0u, 0u, 0u, 0u, 0u};
+    if constexpr (APPLY == APPLY_Q && NR >= 2) {
+#pragma unroll
+        for (int r = 0; r < NR; ++r) count_add(wc, cw[r]);
+    }
     uint32_t v[CH];
     bool bad = false;
 #pragma unroll
     for (int c = 0; c < CH; ++c) {
         const int64_t e = e0 + 128 * (c0 + c) + 4 * lane;
-        const int nv = FULL ? 4 : nvalid4(ne, 128 * (c0 + c) + 4 * lane);
+        const int nv = WHOLE ? 4 : nvalid4(ne, 128 * (c0 + c) + 4 * lane);
         float g4[4] = {gv[c].x, gv[c].y, gv[c].z, gv[c].w};
         WV<TW>& w4 = wv[c];
         const TR(&r4)[4] = rv[c].v;
@@ -231,8 +238,12 @@ __device__ __forceinline__ uint32_t fused_vec_task(const FusedArgs& a, const Hot
             float l4[4];
             if constexpr (APPLY == APPLY_Q) {
                 Counts cnt{0u, 0u, 0u, 0u, 0u};
+                if constexpr (NR >= 2) {
+                    cnt = shfl_counts(wc, 8 * (c0 + c) + (lane >> 2));
+                } else {
 #pragma unroll
-                for (int r = 0; r < NR; ++r) count_add(cnt, __shfl_sync(FULL, cw[r], 8 * (c0 + c) + (lane >> 2)));
+                    for (int r = 0; r < NR; ++r) count_add(cnt, __shfl_sync(FULL, cw[r], 8 * (c0 + c) + (lane >> 2)));
+                }
                 int cq[4];
                 lane_counts(cnt, lane, cq);
 #pragma unroll
