@@ -732,8 +732,8 @@ __device__ __forceinline__ void apply_vec_tile(const ApplyQArgs& a, const K2Hot&
     WV<TW>(&wt)[CH] = L.wt;
     float4(&gt)[CH] = L.gt;
     const int a_on = a_off ? 0 : 1;
-    Counts wc{0u, 0u, 0u, 0u, 0u};  // this lane's word, counts summed over the ranks (NR >= 2)
-    if constexpr (NR >= 2) {
+    Counts wc{0u, 0u, 0u, 0u, 0u};  // this lane's word, counts summed over the ranks (NR > 5)
+    if constexpr (NR > 5) {
 #pragma unroll
         for (int r = 0; r < R; ++r) count_add(wc, wv[r]);
     }
@@ -742,7 +742,7 @@ __device__ __forceinline__ void apply_vec_tile(const ApplyQArgs& a, const K2Hot&
         const int64_t e = e0 + 128 * (c0 + c) + 4 * lane;
         const int nv = WHOLE ? 4 : nvalid4(ne, 128 * (c0 + c) + 4 * lane);
         Counts cnt{0u, 0u, 0u, 0u, 0u};
-        if constexpr (NR >= 2) {
+        if constexpr (NR > 5) {  // (see fused_vec_task)
             cnt = shfl_counts(wc, 8 * (c0 + c) + (lane >> 2));
         } else {
 #pragma unroll

@@ -218,10 +218,12 @@ __device__ __forceinline__ uint32_t fused_vec_task(const FusedArgs& a, const Hot
     // behind the error word's round trip (two dependent trips per task instead of one).
     constexpr bool SINK = CH == 1;
     const int a_on = a_off ? 0 : 1;
-    // several ranks: each lane sums the counts of ITS word over the ranks once (the words of a
-    // chunk are read by 4 lanes each), then a chunk shuffles 5 counters instead of N words
+    // many ranks (N > 5): each lane sums the counts of ITS word over the ranks once (the words
+    // of a chunk are read by 4 lanes each), then a chunk shuffles 5 counters instead of N words.
+    // Fewer ranks shuffle the words: at N = 2 / 4 the 5 shuffles measured slower in the engine
+    // (F 200 vs 186 us at N = 2) although the standalone kernel gained.
     Counts wc{0u, 0u, 0u, 0u, 0u};
-    if constexpr (APPLY == APPLY_Q && NR >= 2) {
+    if constexpr (APPLY == APPLY_Q && NR > 5) {
 #pragma unroll
         for (int r = 0; r < NR; ++r) count_add(wc, cw[r]);
     }
@@ -238,7 +240,7 @@ __device__ __forceinline__ uint32_t fused_vec_task(const FusedArgs& a, const Hot
             float l4[4];
             if constexpr (APPLY == APPLY_Q) {
                 Counts cnt{0u, 0u, 0u, 0u, 0u};
-                if constexpr (NR >= 2) {
+                if constexpr (NR > 5) {
                     cnt = shfl_counts(wc, 8 * (c0 + c) + (lane >> 2));
                 } else {
 #pragma unroll
