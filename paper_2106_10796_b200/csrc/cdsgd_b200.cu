@@ -1,6 +1,7 @@
 // cdsgd_b200.cu — C ABI, launch logic, NCCL exchange and the per-rank step
 // engine of the B200-native CD-SGD hot path. Declarations and the reference
 // interface each entry point replaces: include/cdsgd_b200.h.
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <nccl.h>
 
@@ -1084,6 +1085,40 @@ int p2p_ce_finish(cdsgd_engine* E, cudaStream_t C) {
     return CDSGD_OK;
 }
 
+// Flag publication of the copy-engine phases: a 1-thread k_flags kernel (it can wait up to
+// ~13 us for an SM beside K2/K1 at N=4), or with CDSGD_FLAG_MEMOPS=1 a stream memory
+// operation (cuStreamWriteValue64, whose system-wide fence before the write orders every
+// earlier copy of the stream first; no SM). Measured: memops 436-438 vs 441 Gelem/s at N=4,
+// 247 vs 250 at N=2 — no gain, so the kernel stays the default.
+using StreamWrite64Fn = CUresult (*)(CUstream, CUdeviceptr, cuuint64_t, unsigned int);
+StreamWrite64Fn stream_write64() {
+    static const StreamWrite64Fn fn = [] {
+        const char* e = getenv("CDSGD_FLAG_MEMOPS");
+        if (e == nullptr || atoi(e) == 0) return static_cast<StreamWrite64Fn>(nullptr);
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        if (cudaGetDriverEntryPoint("cuStreamWriteValue64", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            return static_cast<StreamWrite64Fn>(nullptr);
+        return reinterpret_cast<StreamWrite64Fn>(p);
+    }();
+    return fn;
+}
+int publish_flags(const P2PArgs& x, cudaStream_t s) {
+    if (const StreamWrite64Fn fn = stream_write64()) {
+        bool ok = true;
+        for (int r = 0; r < x.nranks && ok; ++r)
+            if (x.publish[r] != nullptr)
+                ok = fn(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(x.publish[r]),
+                        static_cast<cuuint64_t>(x.publish_value), 0) == CUDA_SUCCESS;
+        if (ok) return CDSGD_OK;
+        return fail(CDSGD_ERR_CUDA, "cuStreamWriteValue64 failed (unset CDSGD_FLAG_MEMOPS to use the flag kernel)");
+    }
+    k_flags<<<1, 32, 0, s>>>(x);
+    LAUNCH_CHECK();
+    return CDSGD_OK;
+}
+
 // Peer copies of one copy-engine phase: copy k (dst[k] <- src[k], bytes[k]) on stream xsc[k],
 // forked from and joined back into X, so the transfers to different peers overlap on several
 // copy engines (CDSGD_CE_PARALLEL=1; serially on X by default).
@@ -1144,8 +1179,10 @@ int p2p_ce_allreduce(cdsgd_engine* E, int64_t p, const float* g, cudaStream_t X,
     fr.nranks = nr;
     for (int r = 0; r < nr; ++r) fr.publish[r] = at<uint64_t>(E->peer[r], E->off_gready) + s * nr + me;
     fr.publish_value = static_cast<uint64_t>(p) + 1;
-    k_flags<<<1, 32, 0, X>>>(fr);
-    LAUNCH_CHECK();
+    {
+        const int rc = publish_flags(fr, X);
+        if (rc != CDSGD_OK) return rc;
+    }
     if (E->ce_defer) {  // steps 3-5 are issued by the next step (p2p_ce_finish)
         E->ce_pend.on = true;
         E->ce_pend.p = p;
@@ -1223,8 +1260,10 @@ int p2p_ce_reduce_gather(cdsgd_engine* E, int64_t p, const float* g, cudaStream_
     fd.nranks = nr;
     for (int r = 0; r < nr; ++r) fd.publish[r] = at<uint64_t>(E->peer[r], E->off_wdone) + me;
     fd.publish_value = static_cast<uint64_t>(p) + 1;
-    k_flags<<<1, 32, 0, X>>>(fd);
-    LAUNCH_CHECK();
+    {
+        const int rc = publish_flags(fd, X);
+        if (rc != CDSGD_OK) return rc;
+    }
     P2PArgs w{};  // 5. every rank's shard has landed in my gsum
     w.nranks = nr;
     w.wait_flags = at<const uint64_t>(local, E->off_wdone);
