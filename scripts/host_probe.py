@@ -64,6 +64,36 @@ def main():
     for i in range(N):
         wk._lib.cdsgd_launch_count()
     out["ctypes_noop_us"] = 1e6 * (time.perf_counter() - t0) / N
+    # the standalone fused-round ABI (same kernel, arguments built per call, no engine state)
+    from paper_2106_10796_b200 import _lib
+
+    nw = layout.n_words
+    r = [torch.zeros(n, dtype=torch.float64, device=dev) for _ in range(2)]
+    W = torch.zeros(n, dtype=torch.float64, device=dev)
+    loc = torch.empty(n, device=dev)
+    words = torch.zeros(nw, dtype=torch.int32, device=dev)
+    err = torch.full((2,), -1, dtype=torch.int64, device=dev)
+    lay = layout.handle().ptr
+    ff = wk._lib.cdsgd_fused_round
+    args = [(lay, ptrs[i], r[i].data_ptr(), r[i ^ 1].data_ptr(), _lib.F64, words.data_ptr(), 0.5, err.data_ptr(), 0,
+             W.data_ptr(), _lib.F64, loc.data_ptr(), words.data_ptr(), 1, nw, 0.1, 0.4, 0, None, st) for i in range(2)]
+    for i in range(100):
+        ff(*args[i & 1])
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for i in range(N):
+        ff(*args[i & 1])
+    out["fused_round_abi_us_host"] = 1e6 * (time.perf_counter() - t0) / N
+    torch.cuda.synchronize()
+    x = torch.zeros(1, device=dev)
+    for i in range(100):
+        x.add_(1.0)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for i in range(N):
+        x.add_(1.0)
+    out["torch_tiny_kernel_us_host"] = 1e6 * (time.perf_counter() - t0) / N
+    torch.cuda.synchronize()
     wk.check()
     wk.close()
     print(json.dumps(out), flush=True)
