@@ -219,3 +219,32 @@ def test_weight_drift_envelope(pkg, weights):
     if os.path.isdir(d):
         with open(os.path.join(d, f"drift_envelope_{weights}.json"), "w") as f:
             json.dump(out, f, indent=1)
+
+
+@pytest.mark.parametrize("N", [4, 8])
+def test_half_tile_fused_round_many_ranks_bitwise(pkg, N):
+    """Layouts above the small-layout threshold with several ranks' codes and fp64 W run the
+    fused round on HALF tiles (no register spill; for N > 5 also with per-word count sums):
+    W bitwise against the reference's fp64 W (C port) and residuals bitwise, every round."""
+    from localsim import LocalSim
+
+    _, L, _ = pkg
+    sizes = [2_600_000, 77, 3000]  # > 4,736 tiles: whole-/half-tile tasks, not chunk tasks
+    layout = L.Layout.from_lengths(sizes)
+    n, T, eta = layout.total, 4, 0.1
+    w0 = O.synthetic_weights(11, n)
+    sim = LocalSim(layout, N, w0, k=10_000, alpha=0.5, eta_g=eta, eta_l=0.4, warmup=0, weights="f64")
+    port = cpu_port.CPortEngine(w0.astype(np.float64), sizes, N, k=10_000, alpha=0.5, eta_g=eta, eta_l=0.4)
+    Wref_prev = None
+    for t in range(T):
+        g = grads_of(11, t, N, n)
+        sim.step([torch.from_numpy(g[w]).cuda() for w in range(N)])
+        port.step(g)
+        if t >= 1:
+            assert sim.kernels[-1] == ["F"], sim.kernels[-1]
+            assert np.array_equal(bits(sim.W[0].cpu().numpy()), bits(Wref_prev)), f"W not bitwise after round {t - 1}"
+        for w in range(N):
+            assert np.array_equal(bits(sim.residual(w).cpu().numpy()), bits(port.res[w])), f"residual t={t} w={w}"
+        Wref_prev = port.W.copy()
+    sim.flush()
+    assert np.array_equal(bits(sim.W[0].cpu().numpy()), bits(port.W))
