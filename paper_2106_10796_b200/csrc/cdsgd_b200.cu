@@ -873,6 +873,14 @@ struct cdsgd_engine {
     cudaEvent_t evC = nullptr;
     cudaEvent_t evQ[2] = {nullptr, nullptr};
     cudaEvent_t evX[2] = {nullptr, nullptr};
+    // Split correction apply (CDSGD_SPLIT_APPLY=1): NCCL's share [0, split_off) of a correction
+    // all-reduce ends before the copy engines' all-gather of the rest, so K3 applies that prefix
+    // once evN fires and the rest after evX (0 = not split). Parity-green, measured within noise
+    // (N=4 441/442 -> 446/442, N=2 250 -> 246 Gelem/s: the two halves' tails and the prefix's
+    // HBM traffic beside the all-gather cost what the earlier start gains) -> off by default.
+    cudaEvent_t evN[2] = {nullptr, nullptr};
+    int64_t split_off[2] = {0, 0};
+    bool split_apply = false;
     DecodeTab tab{};
     int exact = 0;
     bool uses_local = false;
@@ -1383,7 +1391,8 @@ int engine_apply(cdsgd_engine* E, int64_t p, bool comp, const float* gp, const f
                                     E->d.eta_local, C);
         return rc;
     }
-    if (nr > 1 && E->xused[p & 1]) CUDA_TRY(cudaStreamWaitEvent(C, E->evX[p & 1], 0));
+    const int64_t soff = nr > 1 && E->xused[p & 1] && !comp ? E->split_off[p & 1] : 0;
+    if (nr > 1 && E->xused[p & 1]) CUDA_TRY(cudaStreamWaitEvent(C, soff > 0 ? E->evN[p & 1] : E->evX[p & 1], 0));
     const int64_t rel = p - E->err_base + 1;
     const uint64_t skip_below = rel <= 0 ? 0ull : (static_cast<uint64_t>(rel) << CDSGD_INDEX_BITS);
     double* gn = gnorm_slot(E, p);
@@ -1421,9 +1430,15 @@ int engine_apply(cdsgd_engine* E, int64_t p, bool comp, const float* gp, const f
     }
     const float* gsum = nr > 1 ? E->d.gsum[p & 1] : gp;
     const long pi = prof_start(E, 2, C);
-    const int rc = launch_apply_full(E->d.weights, E->d.weights_dtype, gsum, nr, E->L->n, E->d.eta_global, gnext, loc,
-                                     E->d.eta_local,
-                                     E->d.err, skip_below, gn, C, clr);
+    int rc = launch_apply_full(E->d.weights, E->d.weights_dtype, gsum, nr, soff > 0 ? soff : E->L->n, E->d.eta_global,
+                               gnext, loc, E->d.eta_local, E->d.err, skip_below, gn, C, clr);
+    if (rc == CDSGD_OK && soff > 0) {  // the copy engines' share, once every rank's shard has landed
+        CUDA_TRY(cudaStreamWaitEvent(C, E->evX[p & 1], 0));
+        const size_t es = E->d.weights_dtype == CDSGD_F64 ? sizeof(double) : sizeof(float);
+        rc = launch_apply_full(static_cast<char*>(E->d.weights) + es * soff, E->d.weights_dtype, gsum + soff, nr,
+                               E->L->n - soff, E->d.eta_global, gnext != nullptr ? gnext + soff : nullptr,
+                               loc != nullptr ? loc + soff : nullptr, E->d.eta_local, E->d.err, skip_below, gn, C);
+    }
     prof_stop(E, pi, C);
     return rc;
 }
@@ -1477,6 +1492,8 @@ extern "C" int cdsgd_engine_create(const cdsgd_engine_desc* d, const cdsgd_layou
         E->reserve_sms = rs != nullptr ? std::max(0, atoi(rs)) : 0;
         const char* pa = getenv("CDSGD_PLAIN_AFTER_AR");
         E->plain_after_ar = pa != nullptr && pa[0] == '1';
+        const char* sa = getenv("CDSGD_SPLIT_APPLY");
+        E->split_apply = sa != nullptr && sa[0] == '1';
         const char* ns = getenv("CDSGD_STATIC_SCHED");
         if (!(ns != nullptr && ns[0] == '1')) {
             if (cudaMalloc(&E->sched, 4 * sizeof(unsigned int)) != cudaSuccess ||
@@ -1507,6 +1524,7 @@ extern "C" int cdsgd_engine_create(const cdsgd_engine_desc* d, const cdsgd_layou
         for (int i = 0; i < 2 && e == cudaSuccess; ++i) {
             e = cudaEventCreateWithFlags(&E->evQ[i], cudaEventDisableTiming);
             if (e == cudaSuccess) e = cudaEventCreateWithFlags(&E->evX[i], cudaEventDisableTiming);
+            if (e == cudaSuccess) e = cudaEventCreateWithFlags(&E->evN[i], cudaEventDisableTiming);
         }
     }
     if (e != cudaSuccess) {
@@ -1729,6 +1747,7 @@ extern "C" int cdsgd_engine_destroy(cdsgd_engine* E) {
     for (int i = 0; i < 2; ++i) {
         if (E->evQ[i]) cudaEventDestroy(E->evQ[i]);
         if (E->evX[i]) cudaEventDestroy(E->evX[i]);
+        if (E->evN[i]) cudaEventDestroy(E->evN[i]);
     }
     if (E->xs) cudaStreamDestroy(E->xs);
     if (E->xs2) cudaStreamDestroy(E->xs2);
@@ -1974,6 +1993,7 @@ extern "C" int cdsgd_engine_step(cdsgd_engine* E, const float* g, void* stream) 
         E->rcur ^= 1;
     }
     // 2. exchange round t on the engine's stream (codes are already delivered when fused)
+    E->split_off[t & 1] = 0;
     E->xused[t & 1] = nr > 1 && (!E->p2p || (!comp && !E->pcorr));
     // the split pays only when the all-reduce overlaps compute: a synchronous round (ssgd,
     // warm-up) waits for it at once, and NCCL alone is faster there (ssgd N=4: 0.57 vs 0.69 ms)
@@ -1981,8 +2001,15 @@ extern "C" int cdsgd_engine_step(cdsgd_engine* E, const float* g, void* stream) 
         // correction all-reduce split between NCCL (stream X, SMs) and the copy engines
         // (stream X2): the copy engines barely contend with the compute kernels
         const int64_t n = E->L->n;
-        const int64_t cnt = std::min<int64_t>(n, static_cast<int64_t>(E->ce_frac * n) / 4 * 4);
-        const int64_t off = n - cnt;
+        int64_t cnt = std::min<int64_t>(n, static_cast<int64_t>(E->ce_frac * n) / 4 * 4);
+        int64_t off = n - cnt;
+        // split apply: NCCL's share ends on a tile boundary (both K3 halves keep the TMA path)
+        const int64_t off_t = off / TILE_ELEMS * TILE_ELEMS;
+        const bool split = E->split_apply && off_t > 0 && (n - off_t) % 4 == 0;
+        if (split) {
+            off = off_t;
+            cnt = n - off;
+        }
         CUDA_TRY(cudaEventRecord(E->evQ[t & 1], C));
         CUDA_TRY(cudaStreamWaitEvent(E->xs, E->evQ[t & 1], 0));
         CUDA_TRY(cudaStreamWaitEvent(E->xs2, E->evQ[t & 1], 0));
@@ -1996,6 +2023,10 @@ extern "C" int cdsgd_engine_step(cdsgd_engine* E, const float* g, void* stream) 
             NCCL_TRY(ncclAllReduce(g, E->d.gsum[t & 1], static_cast<size_t>(off), ncclFloat, ncclSum, E->comm->nccl,
                                    E->xs));
         prof_stop(E, pi, E->xs);
+        if (split) {
+            CUDA_TRY(cudaEventRecord(E->evN[t & 1], E->xs));
+            E->split_off[t & 1] = off;
+        }
         const long pc = prof_start(E, 10, E->xs2);
         rc = p2p_ce_allreduce(E, t, g, E->xs2, off, cnt);
         if (rc != CDSGD_OK) return rc;
