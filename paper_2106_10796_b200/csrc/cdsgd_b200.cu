@@ -1542,23 +1542,35 @@ int64_t p2p_chunk(int32_t nranks, int64_t n) { return (((n + nranks - 1) / nrank
 // Symmetric buffer: codes slot 0 | slot 1 | ready[2][N] | freed[2][N] | W [n] |
 // recv 0 [N][chunk] | recv 1 [N][chunk] | gready[2][N] | gfreed[2][N] | wdone[N] | gpart[2][N] |
 // gsum 0 [n] | gsum 1 [n] | end
+// Alignment of the streamed arrays inside the symmetric buffer (CDSGD_P2P_ALIGN bytes, a power
+// of two >= 256; default 256): W, the staging rows and gsum start on this boundary.
+int64_t p2p_align() {
+    static const int64_t v = [] {
+        const char* e = getenv("CDSGD_P2P_ALIGN");
+        const long long a = e != nullptr ? atoll(e) : 256;
+        return a >= 256 && (a & (a - 1)) == 0 ? static_cast<int64_t>(a) : int64_t(256);
+    }();
+    return v;
+}
 void p2p_offsets(int32_t nranks, int64_t n, int64_t words, int64_t* off /* [14] */) {
+    const int64_t A = p2p_align();
+    auto up = [A](int64_t x) { return (x + A - 1) / A * A; };
     const int64_t flags = align256(2 * nranks * 8);
-    const int64_t recv = align256(4 * static_cast<int64_t>(nranks) * p2p_chunk(nranks, n));
+    const int64_t recv = up(4 * static_cast<int64_t>(nranks) * p2p_chunk(nranks, n));
     off[0] = 0;
     off[1] = align256(static_cast<int64_t>(nranks) * words * 4);
     off[2] = 2 * off[1];
     off[3] = off[2] + flags;
-    off[4] = off[3] + flags;
-    off[5] = off[4] + align256(8 * n);        // W replica (sized for fp64 weights)
+    off[4] = up(off[3] + flags);
+    off[5] = off[4] + up(8 * n);        // W replica (sized for fp64 weights)
     off[6] = off[5] + recv;
     off[7] = off[6] + recv;
     off[8] = off[7] + flags;
     off[9] = off[8] + flags;
     off[10] = off[9] + align256(nranks * 8);
-    off[11] = off[10] + flags;               // gsum 0
-    off[12] = off[11] + align256(4 * n);     // gsum 1
-    off[13] = off[12] + align256(4 * n);     // end
+    off[11] = up(off[10] + flags);      // gsum 0
+    off[12] = off[11] + up(4 * n);      // gsum 1
+    off[13] = off[12] + up(4 * n);      // end
 }
 }  // namespace
 
