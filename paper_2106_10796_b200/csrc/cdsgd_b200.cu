@@ -1655,9 +1655,13 @@ extern "C" int cdsgd_engine_attach_p2p(cdsgd_engine* E, void* const* peer_bases,
     E->d.gsum[1] = reinterpret_cast<float*>(local + E->off_gsum[1]);
     E->d.gathered[0] = reinterpret_cast<uint32_t*>(local + E->off_slot[0]);
     E->d.gathered[1] = reinterpret_cast<uint32_t*>(local + E->off_slot[1]);
-    // the W replica moves into symmetric memory (peers store their W' shards into it)
+    // the W replica moves into symmetric memory when peers store their W' shards into it (the
+    // exact correction); CDSGD_W_SYMMETRIC=1 moves it in every P2P mode (A/B; worker.py follows
+    // the same rule for its view of W)
     void* wsym = local + E->off_W;
-    if (wsym != E->d.weights) {
+    const char* wsm = getenv("CDSGD_W_SYMMETRIC");
+    const bool w_move = exact_correction != 0 || (wsm != nullptr && wsm[0] == '1');
+    if (w_move && wsym != E->d.weights) {
         const size_t wb = E->d.weights_dtype == CDSGD_F64 ? 8 : 4;
         CUDA_TRY(cudaMemcpy(wsym, E->d.weights, wb * E->L->n, cudaMemcpyDeviceToDevice));
         E->d.weights = wsym;

@@ -184,10 +184,12 @@ class CDSGDWorker:
             raise ConfigError("symmetric memory group does not match hp.workers")
         arr = (C.c_void_p * self.world)(*ptrs)
         _lib.check(lib.cdsgd_engine_attach_p2p(self._eng, arr, self.world, int(exact)), "cdsgd_engine_attach_p2p")
-        # the engine moved the W replica into the symmetric buffer (peers write W' shards into it),
+        # with the exact correction the engine moved the W replica into the symmetric buffer (peers
+        # write W' shards into it; CDSGD_W_SYMMETRIC=1: in every P2P mode, the engine's same rule),
         # and the code slots live there too (slot 0 at offset 0, slot 1 at the next 256-B boundary)
-        es = self.W.element_size()
-        self.W = self._symm[w_off:w_off + es * n].view(self.W.dtype)
+        if exact or os.environ.get("CDSGD_W_SYMMETRIC", "0") == "1":
+            es = self.W.element_size()
+            self.W = self._symm[w_off:w_off + es * n].view(self.W.dtype)
         slot = (self.world * nw * 4 + 255) // 256 * 256
         self.gathered = [self._symm[i * slot:i * slot + self.world * nw * 4].view(torch.uint32) for i in range(2)]
         torch.cuda.synchronize(self.device)
